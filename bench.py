@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Trace-transform benchmark (contract: one JSON line from rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1]
+                  [--impl ours|reference] [--sampler 0|1]
+
+Metric: sinogram samples/s = F*A*n per image per second (F = 6 for T0..T5),
+whole job over all ranks.  A "step" is one pass of the hot path over one
+image of the workload:
+  c2 (default, BASELINE.json configs[1]): 1024^2 image, 720 angles, T0..T5;
+     N>1: one image per rank ("image batches sharded", weak scaling), the
+     per-rank feature summaries gathered to rank 0 over NCCL.
+  c3: 4096^2 image, 1440 angles, T0..T5; N>1: orientations sharded across
+     ranks (strong scaling), sinogram slices all-gathered over NCCL.
+  c1: 256^2, 360 angles (the reference's CPU-runnable case).
+`value` times the fused kernel on device-resident inputs (CUDA events on the
+launching stream, L2 flushed between steps, max over ranks); `e2e` times the
+public API (TraceTransform.run_resident: pinned H2D of the image, the launch,
+D2H of sinograms + medians).  `--impl reference` runs the reference's own
+execution engine (oracle/_ref: the gridjit emulator running
+oracle/trace_t05.krn) on a bounded sample, on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c1": dict(n=256, angles=360, full=True, desc="256^2 fp32, 360 angles x 256 lines, T0-T5"),
+    "c2": dict(n=1024, angles=720, full=True, desc="1024^2 fp32, 720 angles x 1024 lines, T0-T5"),
+    "c3": dict(n=4096, angles=1440, full=True, desc="4096^2 fp32, 1440 angles x 4096 lines, T0-T5"),
+}
+FLOPS_PER_TAP = {True: 34, False: 16}  # FMA = 2, in-bounds taps only
+METRIC = "trace-transform sinogram samples/s"
+UNIT = "samples/s"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                mask = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- our arm
+
+def fp32_peak_tflops(torch, tt, stream) -> float:
+    """Measured FFMA throughput of this GPU at the current clocks (roofline denominator)."""
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    blocks, iters = props.multi_processor_count * 8, 4096
+    buf = torch.empty(blocks, device="cuda")
+    from paper_1604_03410_b200._lib import lib
+    for _ in range(2):
+        lib.tt_ffma_probe(buf.data_ptr(), blocks, 64, stream.cuda_stream)
+    best = float("inf")
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lib.tt_ffma_probe(buf.data_ptr(), blocks, iters, stream.cuda_stream)
+        e1.record(stream)
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    flops = blocks * 256.0 * iters * 128 * 2
+    return flops / best / 1e12
+
+
+def load_traffic(workload: str):
+    """dram bytes per launch of the fused kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", f"ncu_{workload}_summary.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return j.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT)
+    except Exception:
+        return None, None
+
+
+def cpu_baseline(wl, seconds_target=12.0):
+    """The oracle port (TTO_SEQ32, OpenMP over lines, all host threads) on a
+    bounded sample of angles of the same workload."""
+    import numpy as np
+
+    import oracle as O
+    import paper_1604_03410_b200 as tt
+    n, A = wl["n"], wl["angles"]
+    img = tt.synth_image(tt.DISK, n)
+    c, s, w = tt.make_tables(n, A)
+    cores = os.cpu_count() or 1
+    a_count, t = 1, 0.0
+    while True:
+        t0 = time.perf_counter()
+        O.transform(img, n, c, s, w, a0=0, a_count=a_count, mode=O.SEQ32, nthreads=cores)
+        t = time.perf_counter() - t0
+        if t >= seconds_target / 4 or a_count >= A:
+            break
+        a_count = min(A, max(a_count * 2, int(a_count * seconds_target / 4 / max(t, 1e-3))))
+    samples = 6 * a_count * n
+    return {"value": samples / t, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle TTO_SEQ32 (sequential fp32, pinned sampler) on {a_count} of {A} angles x {n} "
+                      f"lines of the {wl['desc']} workload, {t:.2f} s wall, OpenMP {cores} threads",
+            "seconds": t}
+
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_1604_03410_b200 as tt
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = WORKLOADS[args.workload]
+    n, A, full = wl["n"], wl["angles"], wl["full"]
+    F = 6 if full else 1
+    strong = args.workload == "c3" and ws > 1
+    a0, a_cnt = (rank * A // ws, (rank + 1) * A // ws - rank * A // ws) if strong else (0, A)
+
+    stream = torch.cuda.Stream()
+    sptr = stream.cuda_stream
+    ctab_h, stab_h, wtab_h = tt.make_tables(n, A)
+    img_h = tt.synth_image(tt.DISK, n, tt.SEEDS[tt.DISK] + (0 if strong else rank))
+    with torch.cuda.stream(stream):
+        img = torch.from_numpy(img_h).cuda()
+        ctab, stab, wtab = (torch.from_numpy(x).cuda() for x in (ctab_h, stab_h, wtab_h))
+        out = torch.empty((a_cnt, F, n), device="cuda")
+        med = torch.empty((a_cnt, 2, n), dtype=torch.int32, device="cuda")
+        flush = torch.empty(int(256 << 20) // 4, device="cuda")  # > 126 MB L2
+        gathered = torch.empty((A, F, n), device="cuda") if strong else None
+        feats = torch.empty((ws, 2, F), device="cuda") if (ws > 1 and not strong) else None
+    tex = None
+    if args.sampler == 1:
+        from paper_1604_03410_b200.trace import image_texture
+        tex = image_texture(img.data_ptr(), n, sptr)
+
+    def step():
+        tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
+                        out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex)
+
+    def exchange():
+        if not dist:
+            return
+        with torch.cuda.stream(stream):
+            if strong:  # the single NCCL gather of sinogram slices (equal shards: A % ws == 0)
+                dist.all_gather_into_tensor(gathered, out)
+            else:       # image-batch sharding: gather per-image feature summaries
+                f = torch.stack([out.sum(dim=(0, 2)), out.amax(dim=(0, 2))])
+                dist.all_gather_into_tensor(feats, f)
+
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+        exchange()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+
+    # ---- timed region (device events per step; L2 flushed between steps) ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    with clocks:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            exchange()
+            ev[i][2].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
+    kern_ms = [e0.elapsed_time(e1) for e0, e1, _ in ev]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    samples_step = F * A * n * (1 if strong else ws)  # whole job per step
+    value = samples_step / (ms_per_step / 1e3)
+
+    # ---- e2e through the public API (host buffers, copies in the timed region) ----
+    ctx = tt.create_context(local)
+    ctx.set_sampler(args.sampler)
+    tr = tt.TraceTransform(ctx, n, A, full=full, a0=a0, a_count=a_cnt)
+    from paper_1604_03410_b200._lib import lib
+    import ctypes as C
+    nb_img, nb_out, nb_med = n * n * 4, a_cnt * F * n * 4, a_cnt * 2 * n * 4
+    hp = [C.c_void_p() for _ in range(3)]
+    for h, nb in zip(hp, (nb_img, nb_out, nb_med)):
+        assert lib.tt_host_alloc(nb, C.byref(h)) == 0
+    h_img = np.ctypeslib.as_array((C.c_float * (n * n)).from_address(hp[0].value)).reshape(n, n)
+    h_img[:] = img_h
+    h_out = np.ctypeslib.as_array((C.c_float * (a_cnt * F * n)).from_address(hp[1].value))
+    h_med = np.ctypeslib.as_array((C.c_int32 * (a_cnt * 2 * n)).from_address(hp[2].value))
+    for _ in range(max(2, args.warmup)):
+        tr.run_resident(h_img, h_out, h_med if full else None)
+    e2e_steps = max(5, min(args.steps, 50))
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        tr.run_resident(h_img, h_out, h_med if full else None)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": samples_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nb_img,
+           "d2h_bytes_per_step": nb_out + (nb_med if full else 0), "ms_per_step": e2e_s * 1e3,
+           "api": "TraceTransform.run_resident -> tt_memcpy_htod / tt_launch(trace_t05) / tt_memcpy_dtoh"}
+    # parity spot check of the e2e output against the device-resident one
+    same = np.array_equal(h_out.reshape(a_cnt, F, n), out.cpu().numpy())
+    tr.free_resident()
+    ctx.destroy()
+    for h in hp:
+        lib.tt_host_free(h)
+
+    # ---- roofline of the fused kernel (rank 0's shard) ----
+    taps = lib.tt_count_inbounds_taps(n, a0, a_cnt, ctab_h.ctypes.data, stab_h.ctypes.data)
+    kern_s = statistics.mean(kern_ms) / 1e3
+    peak = fp32_peak_tflops(torch, tt, stream)
+    achieved = FLOPS_PER_TAP[full] * taps / kern_s / 1e12
+    traffic, traffic_src = load_traffic(args.workload)
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic,
+                "peak_source": "measured in this run: tt_ffma_probe (8 independent FFMA chains x 148*8 CTAs), "
+                               "FP32 is the bound (image L2-resident; no tensor-core work)",
+                "work": f"{FLOPS_PER_TAP[full]} flop per in-bounds tap x {taps} taps (SURVEY.md 8d)",
+                "kernel_ms": kern_s * 1e3, "taps_per_s": taps / kern_s,
+                "hbm_algorithmic_bytes": n * n * 4 + a_cnt * (F + 2) * n * 4,
+                "traffic_source": traffic_src}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.workload == "c3" else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (disk-masked U[0,1) noise, seed 20160412 + rank)",
+            "config": {"workload": args.workload, "desc": wl["desc"], "image": [n, n], "angles": A,
+                       "functionals": "T0-T5" if full else "T0", "sampler": ["ldg", "tex"][args.sampler],
+                       "parallelism": (f"orientations sharded x{ws} + NCCL all_gather" if strong else
+                                       (f"images sharded x{ws} + NCCL feature gather" if ws > 1 else "1 GPU")),
+                       "l2": "flushed (256 MiB memset) between timed steps", "ms_per_image": ms_per_step},
+            "e2e": e2e, "roofline": roofline, "clocks": clocks.summary(),
+            "gpu_launches": args.steps * 1, "e2e_matches_device_result": bool(same)}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl)
+    if tex is not None:
+        from paper_1604_03410_b200.trace import image_texture_destroy
+        image_texture_destroy(tex)
+    if dist:
+        dist.destroy_process_group()
+    return line if rank == 0 else None
+
+
+# ---------------------------------------------------------- reference arm
+
+def run_reference(args, ws, rank):
+    """The reference's own execution engine on a bounded sample (rank 0 only)."""
+    if rank != 0:
+        return None
+    import numpy as np
+
+    import oracle as O
+    import paper_1604_03410_b200 as tt  # noqa: F401 (host inputs only: tables / image)
+    wl = WORKLOADS[args.workload]
+    n, A = wl["n"], wl["angles"]
+    if not os.path.exists(O.TIER2_PATH):
+        return {"impl": "reference", "unavailable": "oracle/_ref/tt_tier2 not built (needs /root/reference)"}
+    cores = os.cpu_count() or 1
+    img = tt.synth_image(tt.DISK, n)
+    c, s, w = tt.make_tables(n, A)
+    lines = int(os.environ.get("TT_REF_LINES", "32"))
+    threads = min(cores, A)
+
+    def one():
+        out, med, rep = O.tier2_sample(img, n, c, s, w, angles=threads, lines=lines, threads=threads)
+        return rep
+
+    for _ in range(args.warmup):
+        one()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        rep = one()
+        times.append(time.perf_counter() - t0)
+    samples = 6 * threads * min(lines, n)
+    t = statistics.mean(times)
+    value = samples / t
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": wl["desc"], "image": [n, n], "angles": A,
+                       "functionals": "T0-T5"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"reference gridjit emulator (cuda_launch of oracle/trace_t05.krn) on "
+                                       f"{threads} angles x {lines} lines x {n} taps per step, one DeviceContext "
+                                       f"per host thread"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sampler", type=int, default=int(os.environ.get("TT_BENCH_SAMPLER", "0")), choices=[0, 1])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local = dist_env()
+    line = run_reference(args, ws, rank) if args.impl == "reference" else run_ours(args, ws, rank, local)
+    if line is not None and rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

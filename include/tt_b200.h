@@ -1,0 +1,249 @@
+/*
+ * tt_b200.h — C ABI of the B200-native trace-transform device
+ * (libtt_b200.so, built from paper_1604_03410_b200/csrc/).
+ *
+ * This is the drop-in boundary: every entry point below replaces one
+ * operation of the reference's driver-style API,
+ *   /root/reference/proj/include/gridjit/driver.hpp  (DeviceContext)
+ *   /root/reference/proj/include/gridjit/emulator.hpp (launch/trap types)
+ * and is exactly what an FFI binding of that API would bind (plain pointers,
+ * sizes and PODs; no C++ or torch types).  The C++ surface of the reference
+ * is restored on top of it, source-compatibly, by include/tt/gridjit_b200.hpp;
+ * INTEGRATION.md shows the ctypes and C++ bindings.
+ *
+ * Differences from the emulated device, all deliberate:
+ *   - module_load reads only the `.module` / `.kernel name(params)` header of
+ *     the VPTX text (/root/reference/proj/include/gridjit/vptx.hpp:398-488) and
+ *     binds each kernel to a native sm_100a implementation registered for that
+ *     exact signature; kernels with no native implementation fail at
+ *     tt_get_function with TT_ERR_FUNCTION_NOT_FOUND.  There is no CPU
+ *     fallback of any kind.
+ *   - launches are stream-ordered on the context's CUDA stream; copies are
+ *     synchronous, so every observable result matches the reference's
+ *     synchronous launch.
+ *   - kernel faults are detected on the host before the launch (buffer extents
+ *     are known) and returned as tt_trap values, like TrapInfo; a trapping
+ *     launch has no device side effects.
+ */
+#ifndef TT_B200_H
+#define TT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TT_ABI_VERSION 1
+
+/* One status per exception class of /root/reference/proj/include/gridjit/errors.hpp. */
+typedef enum tt_status {
+    TT_OK = 0,
+    TT_ERR_CONTEXT_DESTROYED = 1, /* ContextDestroyed   errors.hpp:106-109 */
+    TT_ERR_VPTX_SYNTAX = 2,       /* VptxSyntaxError    errors.hpp:97-102   */
+    TT_ERR_VALIDATION_FAILED = 3, /* ValidationFailed   errors.hpp:111-123 */
+    TT_ERR_FUNCTION_NOT_FOUND = 4,/* FunctionNotFound   errors.hpp:125-128 */
+    TT_ERR_OUT_OF_BOUNDS = 5,     /* OutOfBounds        errors.hpp:130-133 */
+    TT_ERR_DOUBLE_FREE = 6,       /* DoubleFree         errors.hpp:135-138 */
+    TT_ERR_USE_AFTER_FREE = 7,    /* UseAfterFree       errors.hpp:140-143 */
+    TT_ERR_ARGUMENT_MISMATCH = 8, /* ArgumentMismatch   errors.hpp:145-148 */
+    TT_ERR_LAUNCH_CONFIG = 9,     /* LaunchConfigError  errors.hpp:150-153 */
+    TT_ERR_ARITY = 10,            /* ArityError         errors.hpp:46-54    */
+    TT_ERR_CUDA = 11,             /* CUDA runtime failure (no emulator analogue) */
+    TT_ERR_INVALID = 12           /* misuse of the C ABI itself (null pointer, short buffer) */
+} tt_status;
+
+typedef struct tt_ctx tt_ctx; /* DeviceContext, driver.hpp:112 */
+
+/* DeviceCaps, emulator.hpp:55-58 (logical launch limits checked by tt_launch). */
+typedef struct tt_caps {
+    uint32_t max_block_threads; /* default 1024 */
+    uint64_t max_shared_bytes;  /* default 48 KiB */
+} tt_caps;
+
+/* DevicePtr, driver.hpp:45-49: a value handle; base is a synthetic address in
+ * the reference's arena convention (first 4096, 256-B aligned, never reused),
+ * mapped to pooled HBM. */
+typedef struct tt_devptr {
+    uint64_t base;
+    uint64_t length; /* bytes */
+    uint64_t ctx_id;
+} tt_devptr;
+
+/* ModuleHandle / FunctionHandle, driver.hpp:31-43 */
+typedef struct tt_module {
+    uint64_t ctx_id;
+    uint64_t id;
+} tt_module;
+typedef struct tt_function {
+    uint64_t ctx_id;
+    uint64_t id;
+} tt_function;
+
+/* GridConfig, emulator.hpp:42-53 */
+typedef struct tt_grid {
+    uint32_t grid[3];
+    uint32_t block[3];
+    uint64_t shared_bytes_extra;
+} tt_grid;
+
+/* LaunchArg = std::variant<int32_t,int64_t,float,double,DevicePtr>, driver.hpp:52 */
+typedef enum tt_arg_kind { TT_ARG_I32 = 0, TT_ARG_I64 = 1, TT_ARG_F32 = 2, TT_ARG_F64 = 3, TT_ARG_PTR = 4 } tt_arg_kind;
+typedef struct tt_arg {
+    int32_t kind; /* tt_arg_kind */
+    int32_t _pad;
+    union {
+        int32_t i32;
+        int64_t i64;
+        float f32;
+        double f64;
+        tt_devptr ptr;
+    } v;
+} tt_arg;
+
+/* TrapInfo::Kind, emulator.hpp:61-68 */
+typedef enum tt_trap_kind {
+    TT_TRAP_GLOBAL_OUT_OF_BOUNDS = 0,
+    TT_TRAP_SHARED_OUT_OF_BOUNDS = 1,
+    TT_TRAP_USE_OF_FREED_MEMORY = 2,
+    TT_TRAP_DIVISION_BY_ZERO = 3,
+    TT_TRAP_BARRIER_DIVERGENCE = 4,
+    TT_TRAP_EXPLICIT = 5
+} tt_trap_kind;
+
+/* LaunchResult / TrapInfo, emulator.hpp:60-102 (trapped == 0 <=> ok()). */
+typedef struct tt_trap {
+    int32_t trapped;
+    int32_t kind;       /* tt_trap_kind */
+    uint32_t thread[3]; /* 1-indexed, source-language convention */
+    uint32_t block[3];  /* 1-indexed */
+    uint64_t instr_index;
+    int64_t code;
+} tt_trap;
+
+/* Counters scalars, driver.hpp:54-96 (launch_log / events via the calls below). */
+typedef struct tt_counters {
+    uint64_t modules_loaded;
+    uint64_t functions_resolved;
+    uint64_t launches;
+    uint64_t allocs;
+    uint64_t frees;
+    uint64_t bytes_h2d;
+    uint64_t bytes_d2h;
+    uint64_t launch_log_size;
+    uint64_t events_size;
+    uint64_t gpu_kernel_launches; /* native CUDA kernels enqueued (extension) */
+} tt_counters;
+
+/* Counters::Event, driver.hpp:55 */
+typedef enum tt_event {
+    TT_EV_MODULE_LOAD = 0,
+    TT_EV_FUNCTION_RESOLVE = 1,
+    TT_EV_ALLOC = 2,
+    TT_EV_FREE = 3,
+    TT_EV_H2D = 4,
+    TT_EV_D2H = 5,
+    TT_EV_LAUNCH = 6
+} tt_event;
+
+/* ---- library ------------------------------------------------------------ */
+int tt_abi_version(void);
+tt_status tt_device_count(int* out);
+/* Last error text of ctx, or of the calling thread when ctx is NULL. */
+const char* tt_last_error(const tt_ctx* ctx);
+/* Registered native kernels, one rendered Signature per line
+ * (types.hpp:100-113 rendering, e.g. "trace_t05(f32[],i32,...)"). */
+tt_status tt_native_kernels(char* buf, size_t cap, size_t* needed);
+
+/* ---- context (driver.hpp:112-132, 332) -------------------------------------- */
+tt_status tt_ctx_create(int device, const tt_caps* caps, tt_ctx** out); /* create_context */
+tt_status tt_ctx_destroy(tt_ctx* ctx);  /* DeviceContext::destroy: release + poison */
+void tt_ctx_release(tt_ctx* ctx);       /* free the handle object (destroys if alive) */
+tt_status tt_ctx_id(const tt_ctx* ctx, uint64_t* out);
+tt_status tt_ctx_synchronize(tt_ctx* ctx);
+tt_status tt_ctx_stream(tt_ctx* ctx, void** stream_out); /* cudaStream_t for interop */
+tt_status tt_ctx_device(const tt_ctx* ctx, int* device_out);
+/* Extension: image sampler of this context's trace launches:
+ * 0 = global/L1 loads (default), 1 = texture gather (TLD4). */
+tt_status tt_ctx_set_sampler(tt_ctx* ctx, int sampler);
+
+/* ---- modules and functions (driver.hpp:138-177) ------------------------------ */
+tt_status tt_module_load(tt_ctx* ctx, const char* vptx_text, size_t len, tt_module* out);
+tt_status tt_module_unload(tt_ctx* ctx, tt_module m);
+tt_status tt_get_function(tt_ctx* ctx, tt_module m, const char* kernel_name, tt_function* out);
+
+/* ---- memory (driver.hpp:179-217) --------------------------------------------- */
+tt_status tt_mem_alloc(tt_ctx* ctx, uint64_t bytes, tt_devptr* out); /* zero-filled */
+tt_status tt_mem_free(tt_ctx* ctx, tt_devptr p);
+tt_status tt_memcpy_htod(tt_ctx* ctx, tt_devptr dst, const void* src, uint64_t bytes);
+tt_status tt_memcpy_dtoh(tt_ctx* ctx, void* dst, tt_devptr src, uint64_t bytes);
+/* Extension: raw CUDA address of a live allocation (interop; no counter). */
+tt_status tt_mem_device_pointer(tt_ctx* ctx, tt_devptr p, void** out);
+/* Extension: page-locked host staging (fast H2D/D2H); not counted. */
+tt_status tt_host_alloc(uint64_t bytes, void** out);
+tt_status tt_host_free(void* p);
+
+/* ---- launch (driver.hpp:221-247) ----------------------------------------------- */
+tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_arg* args, int nargs,
+                    tt_trap* trap_out);
+
+/* ---- introspection (driver.hpp:251-266) ------------------------------------------ */
+tt_status tt_counters_get(tt_ctx* ctx, tt_counters* out);
+/* Counters::to_json (driver.hpp:78-95) as UTF-8 JSON; *needed includes the NUL. */
+tt_status tt_counters_json(tt_ctx* ctx, char* buf, size_t cap, size_t* needed);
+/* Counters::events (driver.hpp:72-74): one tt_event byte per operation. */
+tt_status tt_events(tt_ctx* ctx, uint8_t* buf, size_t cap, size_t* needed);
+
+/* ---- trace-transform helpers (spec DESIGN.md §2) ------------------------------------ */
+/* Host tables: ctab/stab[a_total], wtab[6*n] (any may be NULL). */
+tt_status tt_make_tables(int n, int a_total, float* ctab, float* stab, float* wtab);
+/* Deterministic synthetic images: kind 0 disk-noise, 1 phantom, 2 sparse. */
+tt_status tt_synth_image(int kind, uint64_t seed, int n, float* img);
+/* Warps per line of the fused kernel for side n (the replay schedule). */
+int tt_schedule_warps(int n);
+/* Largest n the fused T0..T5 kernel supports. */
+int tt_max_full_n(void);
+
+/* In-bounds taps of angles [a0, a0+a_count): per line the exact interval of
+ * t whose rotated point passes the spec §2.1 bounds test, found by bisection
+ * on the same fp32 expressions the kernels evaluate (the algorithmic work
+ * count behind the FLOP roofline). */
+uint64_t tt_count_inbounds_taps(int n, int a0, int a_count, const float* ctab, const float* stab);
+
+/* FP32 roofline probe: enqueue blocks x 256 threads x iters x 128 FFMA on
+ * `stream` (2 flop each); out needs `blocks` floats of device memory. */
+tt_status tt_ffma_probe(float* d_out, int blocks, int iters, void* stream);
+
+/* Raw device-pointer entry (multi-GPU driver, benchmarks): enqueue the fused
+ * kernel for angles [a0, a0+a_count) on `stream` (cudaStream_t; NULL = legacy
+ * default).  out: full ? [a_count][6][n] : [a_count][n]; med may be NULL.
+ * sampler: 0 = global/L1 loads, 1 = texture gather (a cudaArray copy of img
+ * is made and released by this call). */
+typedef struct tt_trace_desc {
+    const float* img;
+    int32_t n;
+    int32_t a0;
+    int32_t a_count;
+    int32_t full;
+    const float* ctab;
+    const float* stab;
+    const float* wtab;
+    float* out;
+    int32_t* med;
+    int32_t sampler;
+    int32_t _pad;
+} tt_trace_desc;
+tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
+
+/* Prepared texture for repeated tt_trace_device calls on one image
+ * (sampler 1 without the per-call copy). */
+typedef struct tt_image_tex tt_image_tex;
+tt_status tt_image_tex_create(const float* d_img, int n, void* stream, tt_image_tex** out);
+tt_status tt_image_tex_destroy(tt_image_tex* t);
+tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,152 @@
+"""ctypes wrapper for the CPU oracle (TEST INFRASTRUCTURE — see tt_oracle.h).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline / reference
+legs import this module; the product package never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtt_oracle.so")
+TIER2_PATH = os.path.join(HERE, "_ref", "tt_tier2")
+TIER2_KRN = os.path.join(HERE, "_ref", "trace_t05.krn")
+
+F64, SEQ32, REPLAY = 0, 1, 2
+DISK, PHANTOM, SPARSE = 0, 1, 2
+SEEDS = {DISK: 20160412, PHANTOM: 7, SPARSE: 11}
+NF = 6
+
+_lib = None
+
+
+def build(force: bool = False) -> None:
+    subprocess.check_call(["make", "-C", HERE, "-s", "libtt_oracle.so"] + (["-B"] if force else []))
+
+
+def build_ref() -> bool:
+    """Compile oracle/_ref/tt_tier2 from the reference sources (container only)."""
+    if not os.path.isdir("/root/reference/proj/include"):
+        return os.path.exists(TIER2_PATH)
+    subprocess.check_call(["make", "-C", HERE, "-s", "ref"])
+    return True
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB_PATH)
+        fp = ctypes.POINTER(ctypes.c_float)
+        ip = ctypes.POINTER(ctypes.c_int32)
+        dp = ctypes.POINTER(ctypes.c_double)
+        L.tto_tables.argtypes = [ctypes.c_int, ctypes.c_int, fp, fp, fp]
+        L.tto_synth.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, fp]
+        L.tto_line_samples.argtypes = [fp, ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_int, fp]
+        L.tto_schedule_warps.argtypes = [ctypes.c_int]
+        L.tto_schedule_warps.restype = ctypes.c_int
+        L.tto_transform.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, ip, dp, dp, ctypes.c_int]
+        L.tto_line_f64.argtypes = [fp, ctypes.c_int, fp, ctypes.c_int, ctypes.c_int, dp, dp, ip]
+        L.tto_check.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
+                                ctypes.c_int, fp, ip, ctypes.c_double, ctypes.c_int, ctypes.c_double, dp, ctypes.c_int]
+        L.tto_check.restype = ctypes.c_long
+        _lib = L
+    return _lib
+
+
+def _p(a, t):
+    return a.ctypes.data_as(ctypes.POINTER(t)) if a is not None else None
+
+
+def _f(a):
+    return _p(a, ctypes.c_float)
+
+
+def tables(n: int, a_total: int):
+    c = np.empty(a_total, np.float32)
+    s = np.empty(a_total, np.float32)
+    w = np.empty(6 * n, np.float32)
+    lib().tto_tables(n, a_total, _f(c), _f(s), _f(w))
+    return c, s, w
+
+
+def synth(kind: int, n: int, seed: int | None = None) -> np.ndarray:
+    img = np.empty((n, n), np.float32)
+    lib().tto_synth(kind, SEEDS[kind] if seed is None else seed, n, _f(img))
+    return img
+
+
+def schedule_warps(n: int) -> int:
+    return lib().tto_schedule_warps(n)
+
+
+def line_samples(img, n, c, s, p):
+    v = np.empty(n, np.float32)
+    lib().tto_line_samples(_f(np.ascontiguousarray(img, np.float32)), n, c, s, p, _f(v))
+    return v
+
+
+def transform(img, n, ctab, stab, wtab, *, a0=0, a_count=None, full=True, mode=F64, W=0, nthreads=0,
+              want64=False):
+    """Returns (out f32 [a][F][n], med i32 [a][2][n] or None, out64, absm)."""
+    a_total = len(ctab)
+    a_count = a_total - a0 if a_count is None else a_count
+    F = NF if full else 1
+    out = np.empty((a_count, F, n), np.float32)
+    med = np.zeros((a_count, 2, n), np.int32) if full else None
+    out64 = np.empty((a_count, F, n), np.float64) if (want64 and mode == F64) else None
+    absm = np.empty((a_count, F, n), np.float64) if (want64 and mode == F64) else None
+    lib().tto_transform(_f(np.ascontiguousarray(img, np.float32)), n, a0, a_count, a_total, _f(ctab), _f(stab),
+                        _f(wtab), int(full), mode, W, _f(out), _p(med, ctypes.c_int32),
+                        _p(out64, ctypes.c_double), _p(absm, ctypes.c_double), nthreads)
+    return out, med, out64, absm
+
+
+def check(img, n, ctab, stab, wtab, gpu_out, gpu_med=None, *, a0=0, full=True, rtol=1e-4, W=0, chain=0.0,
+          nthreads=0):
+    """Spec §2.5 checker. Returns (fails, stats dict)."""
+    gpu_out = np.ascontiguousarray(gpu_out, np.float32)
+    a_count = gpu_out.shape[0]
+    st = np.zeros(4, np.float64)
+    gm = None if gpu_med is None else np.ascontiguousarray(gpu_med, np.int32)
+    fails = lib().tto_check(_f(np.ascontiguousarray(img, np.float32)), n, a0, a_count, len(ctab), _f(ctab),
+                            _f(stab), _f(wtab), int(full), _f(gpu_out), _p(gm, ctypes.c_int32), rtol, W, chain,
+                            _p(st, ctypes.c_double), nthreads)
+    return int(fails), {"worst": float(st[0]), "ties": int(st[1]), "median_bad": int(st[2]),
+                        "lines": int(st[3])}
+
+
+def tier2_sample(img, n, ctab, stab, wtab, *, angles, lines, threads):
+    """Bounded sample for the reference benchmark arm: angles [0, angles),
+    lines p < lines of each, one angle per host thread."""
+    return tier2(img, n, ctab, stab, wtab, a0=0, a_count=angles, threads=threads, lines=lines)
+
+
+def tier2(img, n, ctab, stab, wtab, *, a0=0, a_count=None, threads=1, lines=0):
+    """Run the DSL trace kernel on the reference's emulator (oracle/_ref).
+
+    Returns (out f32 [a][6][n], med i32 [a][2][n], report dict)."""
+    if not os.path.exists(TIER2_PATH):
+        raise FileNotFoundError(TIER2_PATH + " (build with `make -C oracle ref`)")
+    a_count = len(ctab) - a0 if a_count is None else a_count
+    with tempfile.TemporaryDirectory() as d:
+        fin, fout = os.path.join(d, "in.bin"), os.path.join(d, "out.bin")
+        with open(fin, "wb") as f:
+            f.write(np.array([n, len(ctab)], np.int32).tobytes())
+            for arr in (img, ctab, stab, wtab):
+                f.write(np.ascontiguousarray(arr, np.float32).tobytes())
+        r = subprocess.run([TIER2_PATH, fin, fout, str(a0), str(a_count), str(threads), TIER2_KRN, str(lines)],
+                           check=True, capture_output=True, text=True)
+        rep = json.loads(r.stdout.strip().splitlines()[-1])
+        raw = np.fromfile(fout, dtype=np.uint8)
+    nout = a_count * 6 * n * 4
+    out = raw[:nout].view(np.float32).reshape(a_count, 6, n)
+    med = raw[nout:].view(np.int32).reshape(a_count, 2, n)
+    return out, med, rep

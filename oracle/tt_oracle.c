@@ -1,0 +1,523 @@
+/*
+ * tt_oracle.c — CPU restatement of the trace transform. TEST INFRASTRUCTURE
+ * ONLY (see tt_oracle.h): the checker for the B200 product, never shipped on
+ * the product path.
+ *
+ * Spec: DESIGN.md §2 (frozen from SURVEY.md Appendix A; algorithm shape from
+ * per-orientation projections reduced by
+ * T-functionals; reference numeric conventions from
+ * /root/reference/proj/include/gridjit/emulator.hpp:5-20).
+ *
+ * Build: oracle/Makefile (gcc -O2 -ffp-contract=off -fopenmp).  The
+ * -ffp-contract=off flag mirrors /root/reference/proj/CMakeLists.txt:15-16 so
+ * that only the explicit fmaf() calls below are fused.
+ */
+#include "tt_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---------------------------------------------------------------- tables */
+
+/* spec §2.1: theta_a = 2*pi*a/A evaluated in f64, rounded to f32 once. */
+void tto_tables(int n, int a_total, float* ctab, float* stab, float* wtab) {
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int a = 0; a < a_total; ++a) {
+        double th = two_pi * (double)a / (double)a_total;
+        if (ctab) ctab[a] = (float)cos(th);
+        if (stab) stab[a] = (float)sin(th);
+    }
+    if (!wtab) return;
+    /* spec §2.2: w3 = r e^{i5 ln r}, w4 = e^{i3 ln r}, w5 = sqrt(r) e^{i4 ln r}; r=0 -> 0 */
+    for (int r = 0; r < n; ++r) {
+        double w3r = 0, w3i = 0, w4r = 0, w4i = 0, w5r = 0, w5i = 0;
+        if (r >= 1) {
+            double lr = log((double)r);
+            double rr = (double)r, sr = sqrt((double)r);
+            w3r = rr * cos(5.0 * lr); w3i = rr * sin(5.0 * lr);
+            w4r = cos(3.0 * lr);      w4i = sin(3.0 * lr);
+            w5r = sr * cos(4.0 * lr); w5i = sr * sin(4.0 * lr);
+        }
+        wtab[0 * (size_t)n + r] = (float)w3r;
+        wtab[1 * (size_t)n + r] = (float)w3i;
+        wtab[2 * (size_t)n + r] = (float)w4r;
+        wtab[3 * (size_t)n + r] = (float)w4i;
+        wtab[4 * (size_t)n + r] = (float)w5r;
+        wtab[5 * (size_t)n + r] = (float)w5i;
+    }
+}
+
+/* ---------------------------------------------------------------- images */
+
+static uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static double draw01(uint64_t seed, int i, int k) {
+    return (double)(splitmix64(seed ^ (0x1000ull + 16ull * (uint64_t)i + (uint64_t)k)) >> 11) *
+           (1.0 / 9007199254740992.0);
+}
+
+/* spec §2.4 */
+void tto_synth(int kind, uint64_t seed, int n, float* img) {
+    const int64_t n1 = (int64_t)n - 1;
+    double cx[8], cy[8], ra[8], rb[8], cp[8], sp[8], al[8];
+    if (kind == TTO_PHANTOM) {
+        const double o = 0.5 * (double)n1;
+        for (int i = 0; i < 8; ++i) {
+            cx[i] = o + (draw01(seed, i, 0) - 0.5) * 0.5 * (double)n;
+            cy[i] = o + (draw01(seed, i, 1) - 0.5) * 0.5 * (double)n;
+            ra[i] = (0.05 + 0.25 * draw01(seed, i, 2)) * (double)n;
+            rb[i] = (0.05 + 0.25 * draw01(seed, i, 3)) * (double)n;
+            double ph = 3.14159265358979323846 * draw01(seed, i, 4);
+            cp[i] = cos(ph);
+            sp[i] = sin(ph);
+            al[i] = 0.1 + 0.9 * draw01(seed, i, 5);
+        }
+    }
+    for (int row = 0; row < n; ++row) {
+        for (int col = 0; col < n; ++col) {
+            uint64_t h = splitmix64(seed ^ (uint64_t)((int64_t)row * n + col));
+            float u = (float)(h >> 40) * (1.0f / 16777216.0f);
+            int64_t dx = 2 * (int64_t)col - n1, dy = 2 * (int64_t)row - n1;
+            int in_disk = dx * dx + dy * dy <= n1 * n1;
+            float val = 0.0f;
+            if (kind == TTO_DISK) {
+                val = in_disk ? u : 0.0f;
+            } else if (kind == TTO_SPARSE) {
+                val = ((h & 127u) == 0) ? u : 0.0f;
+            } else {
+                double acc = 0.0;
+                for (int i = 0; i < 8; ++i) {
+                    double ex = (double)col - cx[i], ey = (double)row - cy[i];
+                    double xr = ex * cp[i] + ey * sp[i];
+                    double yr = ey * cp[i] - ex * sp[i];
+                    double q = (xr / ra[i]) * (xr / ra[i]) + (yr / rb[i]) * (yr / rb[i]);
+                    if (q <= 1.0) acc += al[i];
+                }
+                val = in_disk ? (float)acc : 0.0f;
+            }
+            img[(size_t)row * n + col] = val;
+        }
+    }
+}
+
+/* --------------------------------------------------------------- sampler */
+
+/* spec §2.1: pinned fmaf forms; truncation == floor because the bounds test
+ * has already established q >= 0. */
+static inline float tap(const float* img, int n, float hi, float qx, float qy) {
+    if (!(qx >= 0.0f && qx < hi && qy >= 0.0f && qy < hi)) return 0.0f;
+    int ix = (int)qx, iy = (int)qy;
+    float fx = qx - (float)ix, fy = qy - (float)iy;
+    const float* r0 = img + (size_t)iy * n + ix;
+    const float* r1 = r0 + n;
+    float top = fmaf(fx, r0[1] - r0[0], r0[0]);
+    float bot = fmaf(fx, r1[1] - r1[0], r1[0]);
+    return fmaf(fy, bot - top, top);
+}
+
+void tto_line_samples(const float* img, int n, float c, float s, int p, float* v) {
+    const float o = (float)(n - 1) * 0.5f;
+    const float hi = (float)(n - 1);
+    const float x = (float)p - o;
+    const float u = fmaf(x, c, o);
+    const float w = fmaf(x, s, o);
+    for (int t = 0; t < n; ++t) {
+        float y = (float)t - o;
+        float qx = fmaf(-y, s, u);
+        float qy = fmaf(y, c, w);
+        v[t] = tap(img, n, hi, qx, qy);
+    }
+}
+
+/* Mirrors tt::schedule_warps (paper_1604_03410_b200/csrc/tt_kernels.cu):
+ * the largest power of two <= n/512, clamped to [1, 16]. */
+int tto_schedule_warps(int n) {
+    int w = n / 512, p = 1;
+    if (w < 1) return 1;
+    while (p * 2 <= w && p < 16) p *= 2;
+    return p;
+}
+
+/* ----------------------------------------------------- f64 truth (§2.5) */
+
+static int median64(const float* v, int n, double S) {
+    double P = 0.0;
+    for (int t = 0; t < n; ++t) {
+        P += (double)v[t];
+        if (2.0 * P >= S) return t;
+    }
+    return 0; /* S == 0 handled by the caller; unreachable otherwise */
+}
+
+void tto_line_f64(const float* v, int n, const float* wtab, int m_force, int mp_force,
+                  double out[6], double absm[6], int32_t med[2]) {
+    float* sv = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+    double S = 0.0, Sp = 0.0;
+    for (int t = 0; t < n; ++t) {
+        sv[t] = sqrtf(v[t]);
+        S += (double)v[t];
+        Sp += (double)sv[t];
+    }
+    int m = (S > 0.0) ? median64(v, n, S) : 0;
+    int mp = (Sp > 0.0) ? median64(sv, n, Sp) : 0;
+    if (m_force >= 0) m = m_force;
+    if (mp_force >= 0) mp = mp_force;
+    const float *w3r = wtab, *w3i = wtab + n, *w4r = wtab + 2 * (size_t)n, *w4i = wtab + 3 * (size_t)n,
+                *w5r = wtab + 4 * (size_t)n, *w5i = wtab + 5 * (size_t)n;
+    double t1 = 0, t2 = 0, a3r = 0, a3i = 0, a4r = 0, a4i = 0, a5r = 0, a5i = 0;
+    double m3 = 0, m4 = 0, m5 = 0;
+    for (int t = m; t < n; ++t) {
+        int r = t - m;
+        double vv = (double)v[t];
+        t1 += (double)r * vv;
+        t2 += (double)r * (double)r * vv;
+        a3r += (double)w3r[r] * vv; a3i += (double)w3i[r] * vv;
+        a4r += (double)w4r[r] * vv; a4i += (double)w4i[r] * vv;
+        m3 += (fabs((double)w3r[r]) + fabs((double)w3i[r])) * vv;
+        m4 += (fabs((double)w4r[r]) + fabs((double)w4i[r])) * vv;
+    }
+    for (int t = mp; t < n; ++t) {
+        int r = t - mp;
+        double vv = (double)sv[t];
+        a5r += (double)w5r[r] * vv; a5i += (double)w5i[r] * vv;
+        m5 += (fabs((double)w5r[r]) + fabs((double)w5i[r])) * vv;
+    }
+    out[0] = S; out[1] = t1; out[2] = t2;
+    out[3] = sqrt(a3r * a3r + a3i * a3i);
+    out[4] = sqrt(a4r * a4r + a4i * a4i);
+    out[5] = sqrt(a5r * a5r + a5i * a5i);
+    if (absm) {
+        absm[0] = S; absm[1] = t1; absm[2] = t2; absm[3] = m3; absm[4] = m4; absm[5] = m5;
+    }
+    if (med) { med[0] = m; med[1] = mp; }
+    free(sv);
+}
+
+/* ----------------------------------------------- sequential fp32 (§2.3) */
+
+static int median32_seq(const float* v, int n, float S) {
+    float P = 0.0f;
+    for (int t = 0; t < n; ++t) {
+        P = P + v[t];
+        if (P + P >= S) return t;
+    }
+    return 0;
+}
+
+static void line_seq32(const float* v, float* sv, int n, const float* wtab, float out[6], int32_t med[2]) {
+    float S = 0.0f, Sp = 0.0f;
+    for (int t = 0; t < n; ++t) {
+        sv[t] = sqrtf(v[t]);
+        S = S + v[t];
+        Sp = Sp + sv[t];
+    }
+    int m = median32_seq(v, n, S);
+    int mp = median32_seq(sv, n, Sp);
+    const float *w3r = wtab, *w3i = wtab + n, *w4r = wtab + 2 * (size_t)n, *w4i = wtab + 3 * (size_t)n,
+                *w5r = wtab + 4 * (size_t)n, *w5i = wtab + 5 * (size_t)n;
+    float a1 = 0, a2 = 0, a3r = 0, a3i = 0, a4r = 0, a4i = 0, a5r = 0, a5i = 0;
+    for (int t = m; t < n; ++t) {
+        int r = t - m;
+        float rf = (float)r, r2 = rf * rf, vv = v[t];
+        a1 = fmaf(rf, vv, a1);
+        a2 = fmaf(r2, vv, a2);
+        a3r = fmaf(w3r[r], vv, a3r); a3i = fmaf(w3i[r], vv, a3i);
+        a4r = fmaf(w4r[r], vv, a4r); a4i = fmaf(w4i[r], vv, a4i);
+    }
+    for (int t = mp; t < n; ++t) {
+        int r = t - mp;
+        float vv = sv[t];
+        a5r = fmaf(w5r[r], vv, a5r); a5i = fmaf(w5i[r], vv, a5i);
+    }
+    out[0] = S; out[1] = a1; out[2] = a2;
+    out[3] = sqrtf(fmaf(a3r, a3r, a3i * a3i));
+    out[4] = sqrtf(fmaf(a4r, a4r, a4i * a4i));
+    out[5] = sqrtf(fmaf(a5r, a5r, a5i * a5i));
+    med[0] = m; med[1] = mp;
+}
+
+/* ------------------------------------------- B200 schedule replay (§3.2) */
+
+/* Warp butterfly: x_l <- x_l + x_{l^off}, off = 16..1 (commutative, so every
+ * lane ends with the same value). */
+static float warp_butterfly(float x[32]) {
+    for (int off = 16; off >= 1; off >>= 1) {
+        float y[32];
+        for (int l = 0; l < 32; ++l) y[l] = x[l] + x[l ^ off];
+        memcpy(x, y, sizeof(y));
+    }
+    return x[0];
+}
+
+/* Kogge-Stone inclusive scan: x_l <- x_{l-d} + x_l for l >= d. */
+static void warp_scan(float x[32]) {
+    for (int d = 1; d < 32; d <<= 1) {
+        float y[32];
+        for (int l = 0; l < 32; ++l) y[l] = (l >= d) ? x[l - d] + x[l] : x[l];
+        memcpy(x, y, sizeof(y));
+    }
+}
+
+/* Slot-strided sum over [0,len) with stride 32W, butterfly per warp,
+ * sequential over warps (kernel pass 1 / pass 2 reduction order). */
+static float replay_strided_sum(const float* v, int len, int W) {
+    const int nslot = 32 * W;
+    float total = 0.0f;
+    for (int w = 0; w < W; ++w) {
+        float x[32];
+        for (int l = 0; l < 32; ++l) {
+            float acc = 0.0f;
+            for (int t = 32 * w + l; t < len; t += nslot) acc = acc + v[t];
+            x[l] = acc;
+        }
+        total = total + warp_butterfly(x);
+    }
+    return total;
+}
+
+static int replay_median(const float* v, int n, float S, int W) {
+    const int nslot = 32 * W;
+    const int K = (n + nslot - 1) / nslot;
+    float E = 0.0f;
+    for (int w = 0; w < W; ++w) {
+        float c[32], inc[32];
+        for (int l = 0; l < 32; ++l) {
+            int k = 32 * w + l;
+            float acc = 0.0f;
+            for (int t = k * K; t < n && t < (k + 1) * K; ++t) acc = acc + v[t];
+            c[l] = acc;
+            inc[l] = acc;
+        }
+        warp_scan(inc);
+        for (int l = 0; l < 32; ++l) {
+            int k = 32 * w + l;
+            float e = (l == 0) ? 0.0f : inc[l - 1];
+            float exc = E + e;
+            float pend = exc + c[l];
+            if (pend + pend >= S) {
+                /* first qualifying slot: rescan its chunk */
+                float q = 0.0f;
+                int last = k * K;
+                for (int t = k * K; t < n && t < (k + 1) * K; ++t) {
+                    q = q + v[t];
+                    float P = exc + q;
+                    last = t;
+                    if (P + P >= S) return t;
+                }
+                return last < n ? last : n - 1;
+            }
+        }
+        E = E + inc[31];
+    }
+    return 0;
+}
+
+static void line_replay(const float* v, float* sv, int n, const float* wtab, int W, int full, float out[6],
+                        int32_t med[2]) {
+    if (full)
+        for (int t = 0; t < n; ++t) sv[t] = sqrtf(v[t]);
+    float S = replay_strided_sum(v, n, W);
+    out[0] = S;
+    if (!full) return;
+    float Sp = replay_strided_sum(sv, n, W);
+    int m = replay_median(v, n, S, W);
+    int mp = replay_median(sv, n, Sp, W);
+    const int R = n - m, Rp = n - mp, Rmax = R > Rp ? R : Rp;
+    const int nslot = 32 * W;
+    const float *w3r = wtab, *w3i = wtab + n, *w4r = wtab + 2 * (size_t)n, *w4i = wtab + 3 * (size_t)n,
+                *w5r = wtab + 4 * (size_t)n, *w5i = wtab + 5 * (size_t)n;
+    float tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int w = 0; w < W; ++w) {
+        float x[8][32];
+        for (int l = 0; l < 32; ++l) {
+            float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int r = 32 * w + l; r < Rmax; r += nslot) {
+                float rf = (float)r, r2 = rf * rf;
+                float vv = (r < R) ? v[m + r] : 0.0f;
+                float ss = (r < Rp) ? sv[mp + r] : 0.0f;
+                a[0] = fmaf(rf, vv, a[0]);
+                a[1] = fmaf(r2, vv, a[1]);
+                a[2] = fmaf(w3r[r], vv, a[2]);
+                a[3] = fmaf(w3i[r], vv, a[3]);
+                a[4] = fmaf(w4r[r], vv, a[4]);
+                a[5] = fmaf(w4i[r], vv, a[5]);
+                a[6] = fmaf(w5r[r], ss, a[6]);
+                a[7] = fmaf(w5i[r], ss, a[7]);
+            }
+            for (int j = 0; j < 8; ++j) x[j][l] = a[j];
+        }
+        for (int j = 0; j < 8; ++j) tot[j] = tot[j] + warp_butterfly(x[j]);
+    }
+    out[1] = tot[0];
+    out[2] = tot[1];
+    out[3] = sqrtf(fmaf(tot[2], tot[2], tot[3] * tot[3]));
+    out[4] = sqrtf(fmaf(tot[4], tot[4], tot[5] * tot[5]));
+    out[5] = sqrtf(fmaf(tot[6], tot[6], tot[7] * tot[7]));
+    med[0] = m;
+    med[1] = mp;
+}
+
+/* ------------------------------------------------------------- transform */
+
+void tto_transform(const float* img, int n, int a0, int a_count, int a_total, const float* ctab,
+                   const float* stab, const float* wtab, int full, int mode, int W, float* out, int32_t* med,
+                   double* out64, double* absm, int nthreads) {
+    (void)a_total;
+    const int F = full ? TTO_NF : 1;
+    if (W <= 0) W = tto_schedule_warps(n);
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    const long lines = (long)a_count * n;
+#pragma omp parallel
+    {
+        float* v = (float*)malloc(sizeof(float) * (size_t)n);
+        float* sv = (float*)malloc(sizeof(float) * (size_t)n);
+#pragma omp for schedule(dynamic, 64)
+        for (long L = 0; L < lines; ++L) {
+            const int ai = (int)(L / n), p = (int)(L % n), a = a0 + ai;
+            tto_line_samples(img, n, ctab[a], stab[a], p, v);
+            float o32[6] = {0, 0, 0, 0, 0, 0};
+            int32_t md[2] = {0, 0};
+            if (mode == TTO_F64) {
+                double o64[6], am[6];
+                if (full) {
+                    tto_line_f64(v, n, wtab, -1, -1, o64, am, md);
+                } else {
+                    double S = 0.0;
+                    for (int t = 0; t < n; ++t) S += (double)v[t];
+                    o64[0] = S;
+                    am[0] = S;
+                }
+                for (int f = 0; f < F; ++f) {
+                    o32[f] = (float)o64[f];
+                    if (out64) out64[((size_t)ai * F + f) * n + p] = o64[f];
+                    if (absm) absm[((size_t)ai * F + f) * n + p] = am[f];
+                }
+            } else if (mode == TTO_SEQ32) {
+                if (full) {
+                    line_seq32(v, sv, n, wtab, o32, md);
+                } else {
+                    float S = 0.0f;
+                    for (int t = 0; t < n; ++t) S = S + v[t];
+                    o32[0] = S;
+                }
+            } else {
+                line_replay(v, sv, n, wtab, W, full, o32, md);
+            }
+            for (int f = 0; f < F; ++f) out[((size_t)ai * F + f) * n + p] = o32[f];
+            if (med && full) {
+                med[((size_t)ai * 2 + 0) * n + p] = md[0];
+                med[((size_t)ai * 2 + 1) * n + p] = md[1];
+            }
+        }
+        free(v);
+        free(sv);
+    }
+}
+
+/* --------------------------------------------------------------- checker */
+
+/* Is m an eps-median of v (f64 prefix)?  spec §2.5 */
+static int is_eps_median(const float* v, int n, int m, double eps) {
+    if (m < 0 || m >= n) return 0;
+    double S = 0.0;
+    for (int t = 0; t < n; ++t) S += (double)v[t];
+    if (S == 0.0) return m == 0;
+    double P = 0.0, Pprev = 0.0;
+    for (int t = 0; t <= m; ++t) {
+        Pprev = P;
+        P += (double)v[t];
+    }
+    int reaches = 2.0 * P >= S * (1.0 - eps);
+    int not_before = (m == 0) || (2.0 * Pprev < S * (1.0 + eps));
+    return reaches && not_before;
+}
+
+long tto_check(const float* img, int n, int a0, int a_count, int a_total, const float* ctab, const float* stab,
+               const float* wtab, int full, const float* gpu_out, const int32_t* gpu_med, double rtol, int W,
+               double chain, double* stats, int nthreads) {
+    (void)a_total;
+    const int F = full ? TTO_NF : 1;
+    if (W <= 0) W = tto_schedule_warps(n);
+    const int K = (n + 32 * W - 1) / (32 * W);
+    /* fp32 chain length of the GPU schedule: slot partial + butterfly + warps
+     * (callers checking a sequential fp32 result pass chain = n) */
+    if (chain <= 0.0) chain = (double)K + 5.0 + (double)W + 4.0;
+    const double u = 1.0 / 16777216.0;
+    const double atol_c = 2.0 * chain * u;
+    const double eps = 2.0 * chain * u; /* median tie window */
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    const long lines = (long)a_count * n;
+    long fails = 0, ties = 0, medbad = 0;
+    double worst = 0.0;
+#pragma omp parallel reduction(+ : fails, ties, medbad) reduction(max : worst)
+    {
+        float* v = (float*)malloc(sizeof(float) * (size_t)n);
+        float* sv = (float*)malloc(sizeof(float) * (size_t)n);
+#pragma omp for schedule(dynamic, 64)
+        for (long L = 0; L < lines; ++L) {
+            const int ai = (int)(L / n), p = (int)(L % n), a = a0 + ai;
+            tto_line_samples(img, n, ctab[a], stab[a], p, v);
+            double o64[6], am[6];
+            int32_t md[2] = {0, 0};
+            if (full) {
+                tto_line_f64(v, n, wtab, -1, -1, o64, am, md);
+                if (gpu_med) {
+                    int gm = gpu_med[((size_t)ai * 2 + 0) * n + p];
+                    int gmp = gpu_med[((size_t)ai * 2 + 1) * n + p];
+                    int ok_m = (gm == md[0]), ok_mp = (gmp == md[1]);
+                    if (!ok_m || !ok_mp) {
+                        for (int t = 0; t < n; ++t) sv[t] = sqrtf(v[t]);
+                        if (!ok_m) ok_m = is_eps_median(v, n, gm, eps);
+                        if (!ok_mp) ok_mp = is_eps_median(sv, n, gmp, eps);
+                        if (ok_m && ok_mp) {
+                            ++ties;
+                            tto_line_f64(v, n, wtab, gm, gmp, o64, am, md);
+                        } else {
+                            ++medbad;
+                            ++fails;
+                            continue;
+                        }
+                    }
+                }
+            } else {
+                double S = 0.0;
+                for (int t = 0; t < n; ++t) S += (double)v[t];
+                o64[0] = S;
+                am[0] = S;
+            }
+            for (int f = 0; f < F; ++f) {
+                double g = (double)gpu_out[((size_t)ai * F + f) * n + p];
+                double tol = rtol * fabs(o64[f]) + atol_c * am[f] + 1e-30;
+                double e = fabs(g - o64[f]) / tol;
+                if (!(e <= 1.0)) ++fails; /* NaN fails too */
+                if (e > worst || e != e) worst = (e != e) ? 1e300 : e;
+            }
+        }
+        free(v);
+        free(sv);
+    }
+    if (stats) {
+        stats[0] = worst;
+        stats[1] = (double)ties;
+        stats[2] = (double)medbad;
+        stats[3] = (double)lines;
+    }
+    return fails;
+}

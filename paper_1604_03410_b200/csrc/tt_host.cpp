@@ -1,0 +1,177 @@
+// tt_host.cpp — host-side inputs of the trace transform (product side):
+// angle/weight tables and the deterministic synthetic images of DESIGN.md
+// §2.1-2.4.  These are inputs the caller hands to the device kernels (the
+// reference-style DSL kernel takes ctab/stab as array arguments, SURVEY.md
+// Appendix B); the independent restatement in oracle/tt_oracle.c checks them
+// bit-for-bit (tests/test_host_inputs.py).
+//
+// Compiled with -ffp-contract=off (like /root/reference/proj/CMakeLists.txt:15-16)
+// so every f64 expression rounds exactly as written.
+#include <cmath>
+#include <cstdint>
+#include <cstddef>
+
+#include "tt_b200.h"
+
+namespace {
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+constexpr double kPi = 3.14159265358979323846;
+
+std::uint64_t mix64(std::uint64_t x) {
+    std::uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Uniform [0,1) f64 for parameter k of ellipse i.
+double param01(std::uint64_t seed, int i, int k) {
+    const std::uint64_t key = seed ^ (0x1000ull + 16ull * std::uint64_t(i) + std::uint64_t(k));
+    return double(mix64(key) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+struct Ellipse {
+    double cx, cy, ra, rb, cphi, sphi, alpha;
+};
+
+}  // namespace
+
+extern "C" tt_status tt_make_tables(int n, int a_total, float* ctab, float* stab, float* wtab) {
+    if (n < 0 || a_total < 0) return TT_ERR_INVALID;
+    for (int a = 0; a < a_total; ++a) {
+        const double theta = kTwoPi * double(a) / double(a_total);
+        if (ctab) ctab[a] = float(std::cos(theta));
+        if (stab) stab[a] = float(std::sin(theta));
+    }
+    if (wtab == nullptr) return TT_OK;
+    const std::size_t N = std::size_t(n);
+    for (int r = 0; r < n; ++r) {
+        double re3 = 0, im3 = 0, re4 = 0, im4 = 0, re5 = 0, im5 = 0;
+        if (r > 0) {
+            const double rr = double(r);
+            const double lg = std::log(rr);
+            const double sq = std::sqrt(rr);
+            re3 = rr * std::cos(5.0 * lg);
+            im3 = rr * std::sin(5.0 * lg);
+            re4 = std::cos(3.0 * lg);
+            im4 = std::sin(3.0 * lg);
+            re5 = sq * std::cos(4.0 * lg);
+            im5 = sq * std::sin(4.0 * lg);
+        }
+        wtab[r] = float(re3);
+        wtab[N + r] = float(im3);
+        wtab[2 * N + r] = float(re4);
+        wtab[3 * N + r] = float(im4);
+        wtab[4 * N + r] = float(re5);
+        wtab[5 * N + r] = float(im5);
+    }
+    return TT_OK;
+}
+
+extern "C" tt_status tt_synth_image(int kind, std::uint64_t seed, int n, float* img) {
+    if (n < 0 || img == nullptr || kind < 0 || kind > 2) return TT_ERR_INVALID;
+    const std::int64_t nm1 = std::int64_t(n) - 1;
+    Ellipse el[8];
+    if (kind == 1) {
+        const double centre = 0.5 * double(nm1);
+        for (int i = 0; i < 8; ++i) {
+            el[i].cx = centre + (param01(seed, i, 0) - 0.5) * 0.5 * double(n);
+            el[i].cy = centre + (param01(seed, i, 1) - 0.5) * 0.5 * double(n);
+            el[i].ra = (0.05 + 0.25 * param01(seed, i, 2)) * double(n);
+            el[i].rb = (0.05 + 0.25 * param01(seed, i, 3)) * double(n);
+            const double phi = kPi * param01(seed, i, 4);
+            el[i].cphi = std::cos(phi);
+            el[i].sphi = std::sin(phi);
+            el[i].alpha = 0.1 + 0.9 * param01(seed, i, 5);
+        }
+    }
+    for (std::int64_t y = 0; y < n; ++y) {
+        const std::int64_t ddy = 2 * y - nm1;
+        for (std::int64_t x = 0; x < n; ++x) {
+            const std::uint64_t h = mix64(seed ^ std::uint64_t(y * n + x));
+            const float noise = float(h >> 40) * (1.0f / 16777216.0f);
+            const std::int64_t ddx = 2 * x - nm1;
+            const bool disk = ddx * ddx + ddy * ddy <= nm1 * nm1;
+            float value = 0.0f;
+            switch (kind) {
+                case 0: value = disk ? noise : 0.0f; break;
+                case 2: value = (h & 127u) == 0 ? noise : 0.0f; break;
+                default: {
+                    double sum = 0.0;
+                    for (const Ellipse& e : el) {
+                        const double dx = double(x) - e.cx, dy = double(y) - e.cy;
+                        const double xr = dx * e.cphi + dy * e.sphi;
+                        const double yr = dy * e.cphi - dx * e.sphi;
+                        const double q = (xr / e.ra) * (xr / e.ra) + (yr / e.rb) * (yr / e.rb);
+                        if (q <= 1.0) sum += e.alpha;
+                    }
+                    value = disk ? float(sum) : 0.0f;
+                }
+            }
+            img[std::size_t(y) * std::size_t(n) + std::size_t(x)] = value;
+        }
+    }
+    return TT_OK;
+}
+
+namespace {
+
+// The kernels' fp32 line geometry (spec §2.1), evaluated on the host.
+struct LineGeom {
+    float o, hi, u, w, c, s;
+    LineGeom(int n, float c_, float s_, int p) : c(c_), s(s_) {
+        o = float(n - 1) * 0.5f;
+        hi = float(n - 1);
+        const float x = float(p) - o;
+        u = std::fmaf(x, c, o);
+        w = std::fmaf(x, s, o);
+    }
+    bool inside(int t) const {
+        const float y = float(t) - o;
+        const float qx = std::fmaf(-y, s, u), qy = std::fmaf(y, c, w);
+        return qx >= 0.0f && qx < hi && qy >= 0.0f && qy < hi;
+    }
+};
+
+// First t in [lo, hi) with pred(t) == want given pred is monotone; hi if none.
+template <class P>
+int first_switch(int lo, int hi, bool want, P pred) {
+    while (lo < hi) {
+        const int mid = lo + (hi - lo) / 2;
+        if (pred(mid) == want) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+}  // namespace
+
+extern "C" std::uint64_t tt_count_inbounds_taps(int n, int a0, int a_count, const float* ctab, const float* stab) {
+    if (n < 1 || a_count < 1 || !ctab || !stab) return 0;
+    std::uint64_t total = 0;
+    for (int a = a0; a < a0 + a_count; ++a) {
+        for (int p = 0; p < n; ++p) {
+            const LineGeom g(n, ctab[a], stab[a], p);
+            // Each of the four half-plane tests is monotone in t, so the inside
+            // set is one interval [t_lo, t_hi); find a member by sampling, then
+            // bisect both ends.
+            int member = -1;
+            const int probes = 64;
+            for (int k = 0; k <= probes && member < 0; ++k) {
+                const int t = int((long long)(n - 1) * k / probes);
+                if (g.inside(t)) member = t;
+            }
+            if (member < 0) {  // thin intersection: fall back to a scan
+                int cnt = 0;
+                for (int t = 0; t < n; ++t) cnt += g.inside(t);
+                total += std::uint64_t(cnt);
+                continue;
+            }
+            const int lo = first_switch(0, member, true, [&](int t) { return g.inside(t); });
+            const int hi = first_switch(member, n, false, [&](int t) { return g.inside(t); });
+            total += std::uint64_t(hi - lo);
+        }
+    }
+    return total;
+}

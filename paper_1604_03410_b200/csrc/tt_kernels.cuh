@@ -1,0 +1,77 @@
+// tt_kernels.cuh — launch interface of the sm_100a trace-transform kernels.
+//
+// The path: rotate the image through every orientation and reduce each line
+// (a, p) with the T-functionals (arXiv 1604.03410 §7,
+// /root/reference/PAPER.md:810-829).  Semantics: DESIGN.md §2.  The
+// reference executes this path on its emulated device through
+// DeviceContext::launch -> run_kernel
+// (/root/reference/proj/include/gridjit/driver.hpp:221-247,
+// emulator.hpp:747-793); these kernels replace that engine.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tt {
+
+constexpr int kNumF = 6;  // T0..T5
+
+enum class Sampler : int {
+    Global = 0,   // 4 x LDG through L1 (row-major image in HBM/L2)
+    Texture = 1,  // 1 x TLD4 (tex2Dgather) on a block-linear cudaArray copy
+};
+
+struct TraceArgs {
+    const float* img = nullptr;   // [n][n] row-major (Sampler::Global)
+    cudaTextureObject_t tex = 0;  // same image as a 2-D texture (Sampler::Texture)
+    int n = 0;                    // image side == line length == lines per angle
+    int a0 = 0;                   // first angle (index into ctab/stab)
+    int a_count = 0;              // angles in this launch
+    const float* ctab = nullptr;  // [A_total] cos(theta_a), f64 -> f32 on host
+    const float* stab = nullptr;  // [A_total] sin(theta_a)
+    const float* wtab = nullptr;  // [6][n] planar complex weight tables (spec §2.2)
+    float* out = nullptr;         // full: [a_count][6][n]; T0-only: [a_count][n]
+    int32_t* med = nullptr;       // full: [a_count][2][n] (m, m'), may be null
+    bool full = true;             // T0..T5 (else T0 / Radon only)
+    Sampler sampler = Sampler::Global;
+};
+
+// Warps per line of the fused kernel for side n — part of the reduction
+// schedule that oracle/tt_oracle.c TTO_REPLAY mirrors.
+int schedule_warps(int n);
+
+// Largest n the fused T0-T5 kernel supports (line buffer must fit in smem).
+int max_full_n();
+
+// Enqueue the fused kernel on `stream`.  Returns cudaSuccess or the launch
+// error.  Args must already be validated (sizes, n range).
+cudaError_t launch_trace(const TraceArgs& a, cudaStream_t stream);
+
+// Number of kernel launches launch_trace() issues (for gpu_launches claims).
+int trace_launch_count(const TraceArgs& a);
+
+// Native stand-ins for the reference's sample kernels (boundary tests):
+// c[i] = a[i] + b[i], i = block + thread * blocks (0-based form of
+// /root/reference/proj/kernels/vadd.krn:3-6).  elem: 4 (f32/i32) or 8 (f64/i64).
+enum class ElemKind : int { F32 = 0, F64 = 1, I32 = 2, I64 = 3 };
+cudaError_t launch_vadd(ElemKind k, const void* a, const void* b, void* c, uint64_t count, cudaStream_t s);
+
+// a[i] *= k for i < count (/root/reference/proj/kernels/scale.krn:2-5).
+cudaError_t launch_scale_f32(float* a, float k, uint64_t count, cudaStream_t s);
+
+// b[i] = a[i] (copy, /root/reference/proj/tests/test_autolaunch.cpp:26-28) and
+// out[i] = in[i] + out[i] (add_to, test_autolaunch.cpp:145) for i < count.
+cudaError_t launch_copy_f32(const float* a, float* b, uint64_t count, cudaStream_t s);
+cudaError_t launch_add_to_f32(const float* in, float* out, uint64_t count, cudaStream_t s);
+
+// Texture object over a cudaArray holding a copy of img (caller owns both).
+cudaError_t make_image_texture(const float* img, int n, cudaStream_t s, cudaArray_t* arr,
+                               cudaTextureObject_t* tex);
+
+// FP32 roofline probe: blocks x 256 threads x iters x 128 FFMA (2 flop each).
+cudaError_t launch_ffma_probe(float* out, int blocks, int iters, cudaStream_t s);
+
+// Writes a buffer larger than L2 (timing hygiene between bench iterations).
+cudaError_t launch_l2_flush(void* buf, uint64_t bytes, cudaStream_t s);
+
+}  // namespace tt

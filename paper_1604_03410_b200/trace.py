@@ -1,0 +1,165 @@
+"""Trace-transform entry points on top of the drop-in API.
+
+``TraceTransform`` is the call a user of the reference makes for this path:
+the DSL kernel ``trace_t05(img, n, ctab, stab, wtab, out, med, a0)``
+(oracle/trace_t05.krn; grid = (angles, ceil(n/B)), block = (B)) launched
+through ``cuda_launch`` — here bound to the fused sm_100a kernel.
+``trace_device`` is the raw device-pointer entry used by the multi-GPU
+driver and the device-resident benchmark leg.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib
+from .api import (DeviceContext, GridConfig, KernelAst, _check, cu_in, cu_out, cuda_launch)
+
+DISK, PHANTOM, SPARSE = 0, 1, 2
+SEEDS = {DISK: 20160412, PHANTOM: 7, SPARSE: 11}
+NF = 6
+
+TRACE_T05 = KernelAst("trace_t05", ["img", "n", "ctab", "stab", "wtab", "out", "med", "a0"])
+RADON = KernelAst("radon", ["img", "n", "ctab", "stab", "out", "a0"])
+
+
+def make_tables(n: int, a_total: int):
+    """ctab, stab [a_total] and wtab [6n]."""
+    c = np.empty(a_total, np.float32)
+    s = np.empty(a_total, np.float32)
+    w = np.empty(6 * n, np.float32)
+    _check(lib.tt_make_tables(n, a_total, c.ctypes.data, s.ctypes.data, w.ctypes.data))
+    return c, s, w
+
+
+def synth_image(kind: int, n: int, seed: int | None = None) -> np.ndarray:
+    img = np.empty((n, n), np.float32)
+    _check(lib.tt_synth_image(kind, SEEDS[kind] if seed is None else seed, n, img.ctypes.data))
+    return img
+
+
+def schedule_warps(n: int) -> int:
+    return lib.tt_schedule_warps(n)
+
+
+def max_full_n() -> int:
+    return lib.tt_max_full_n()
+
+
+def launch_config(n: int, angles: int, block: int = 256) -> GridConfig:
+    b = min(block, max(n, 1))
+    return GridConfig((angles, (n + b - 1) // b, 1), (b, 1, 1))
+
+
+class TraceTransform:
+    """Sinograms T0..T5 (or T0 only) of n x n images over `angles` orientations.
+
+    ``__call__(img)`` is the reference-style one-call flow (cuda_launch:
+    alloc, upload, launch, download, free).  ``run_resident(img)`` keeps the
+    tables and output buffers on the device between calls and moves only the
+    image in and the sinograms out (the e2e benchmark path)."""
+
+    def __init__(self, ctx: DeviceContext, n: int, angles: int, full: bool = True, a0: int = 0,
+                 a_count: int | None = None):
+        self.ctx, self.n, self.angles, self.full = ctx, n, angles, full
+        self.a0 = a0
+        self.a_count = angles - a0 if a_count is None else a_count
+        self.ctab, self.stab, self.wtab = make_tables(n, angles)
+        self.F = NF if full else 1
+        self.cfg = launch_config(n, self.a_count)
+        self._res = None
+
+    def out_shape(self):
+        return (self.a_count, self.F, self.n)
+
+    def __call__(self, img: np.ndarray):
+        img = np.ascontiguousarray(img, np.float32)
+        out = np.empty(self.out_shape(), np.float32)
+        if self.full:
+            med = np.empty((self.a_count, 2, self.n), np.int32)
+            rep = cuda_launch(self.ctx, TRACE_T05, self.cfg,
+                              [cu_in(img), np.int32(self.n), cu_in(self.ctab), cu_in(self.stab), cu_in(self.wtab),
+                               cu_out(out), cu_out(med), np.int32(self.a0)])
+        else:
+            med = None
+            rep = cuda_launch(self.ctx, RADON, self.cfg,
+                              [cu_in(img), np.int32(self.n), cu_in(self.ctab), cu_in(self.stab), cu_out(out),
+                               np.int32(self.a0)])
+        if not rep.ok():
+            raise RuntimeError(f"trace launch trapped: {rep.trap}")
+        return out, med, rep
+
+    # ---- device-resident flow --------------------------------------------------
+    def _resident(self):
+        if self._res is None:
+            ctx = self.ctx
+            r = {"img": ctx.mem_alloc(self.n * self.n * 4), "ctab": ctx.mem_alloc(self.ctab.nbytes),
+                 "stab": ctx.mem_alloc(self.stab.nbytes), "wtab": ctx.mem_alloc(self.wtab.nbytes),
+                 "out": ctx.mem_alloc(int(np.prod(self.out_shape())) * 4),
+                 "med": ctx.mem_alloc(self.a_count * 2 * self.n * 4)}
+            ctx.memcpy_htod(r["ctab"], self.ctab)
+            ctx.memcpy_htod(r["stab"], self.stab)
+            ctx.memcpy_htod(r["wtab"], self.wtab)
+            kern = TRACE_T05 if self.full else RADON
+            types = ([(True, "f32"), (False, "i32"), (True, "f32"), (True, "f32"), (True, "f32"), (True, "f32"),
+                      (True, "i32"), (False, "i32")] if self.full else
+                     [(True, "f32"), (False, "i32"), (True, "f32"), (True, "f32"), (True, "f32"), (False, "i32")])
+            from .api import render_module
+            mh = ctx.module_load(render_module(kern, types, kern.name + "$resident"))
+            r["fn"] = ctx.get_function(mh, kern.name)
+            self._res = r
+        return self._res
+
+    def launch_resident(self):
+        """Launch on the resident buffers (image already uploaded)."""
+        r = self._resident()
+        if self.full:
+            args = [r["img"], np.int32(self.n), r["ctab"], r["stab"], r["wtab"], r["out"], r["med"],
+                    np.int32(self.a0)]
+        else:
+            args = [r["img"], np.int32(self.n), r["ctab"], r["stab"], r["out"], np.int32(self.a0)]
+        res = self.ctx.launch(r["fn"], self.cfg, args)
+        if not res.ok():
+            raise RuntimeError(f"trace launch trapped: {res.trap}")
+
+    def run_resident(self, img_host, out_host, med_host=None):
+        """H2D image -> fused kernel -> D2H sinograms (+ medians)."""
+        r = self._resident()
+        self.ctx.memcpy_htod(r["img"], img_host, self.n * self.n * 4)
+        self.launch_resident()
+        self.ctx.memcpy_dtoh(out_host, r["out"], int(np.prod(self.out_shape())) * 4)
+        if med_host is not None and self.full:
+            self.ctx.memcpy_dtoh(med_host, r["med"], self.a_count * 2 * self.n * 4)
+
+    def resident_ptr(self, name: str) -> int:
+        return self.ctx.device_pointer(self._resident()[name])
+
+    def free_resident(self):
+        if self._res is not None:
+            for k in ("img", "ctab", "stab", "wtab", "out", "med"):
+                self.ctx.mem_free(self._res[k])
+            self._res = None
+
+
+def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, stab_ptr: int, wtab_ptr: int,
+                 out_ptr: int, med_ptr: int = 0, full: bool = True, sampler: int = 0, stream: int = 0,
+                 tex=None) -> None:
+    """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex)."""
+    d = _lib.TraceDesc(img_ptr, n, a0, a_count, int(full), ctab_ptr, stab_ptr, wtab_ptr or None, out_ptr,
+                       med_ptr or None, sampler, 0)
+    if tex is not None:
+        _check(lib.tt_trace_device_tex(C.byref(d), tex, C.c_void_p(stream)))
+    else:
+        _check(lib.tt_trace_device(C.byref(d), C.c_void_p(stream)))
+
+
+def image_texture(img_ptr: int, n: int, stream: int = 0):
+    t = C.c_void_p()
+    _check(lib.tt_image_tex_create(C.c_void_p(img_ptr), n, C.c_void_p(stream), C.byref(t)))
+    return t
+
+
+def image_texture_destroy(t) -> None:
+    lib.tt_image_tex_destroy(t)

@@ -1,0 +1,160 @@
+"""Parity of the sm_100a trace kernels with the CPU oracle (spec DESIGN.md §2.5).
+
+Every case is launched through the drop-in path (cuda_launch of the
+trace_t05 / radon signatures on a DeviceContext) and checked two ways:
+  1. bit-exact (sinograms and median indices) against the oracle's replay of
+     the kernel's reduction schedule (TTO_REPLAY);
+  2. against the f64 truth within rtol 1e-4 plus the condition-aware floor,
+     medians exact except eps-ties (north_star's tolerance).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1604_03410_b200 as tt
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [  # (n, A, kind)
+    (1, 3, tt.DISK), (2, 4, tt.DISK), (16, 8, tt.DISK), (31, 7, tt.PHANTOM), (33, 5, tt.SPARSE),
+    (100, 13, tt.SPARSE), (128, 24, tt.DISK), (255, 9, tt.PHANTOM), (256, 360, tt.DISK),  # C1
+    (300, 20, tt.PHANTOM), (512, 16, tt.SPARSE), (1000, 8, tt.DISK), (1024, 16, tt.PHANTOM),
+    (1536, 5, tt.DISK), (2048, 6, tt.SPARSE), (4096, 3, tt.DISK), (8192, 2, tt.PHANTOM), (16384, 1, tt.DISK),
+]
+
+
+@pytest.fixture(scope="module")
+def ctx(gpu):
+    c = tt.create_context(gpu)
+    yield c
+    c.destroy()
+
+
+def _bitwise_equal(a, b):
+    return np.array_equal(np.ascontiguousarray(a).view(np.uint32), np.ascontiguousarray(b).view(np.uint32))
+
+
+def _run(ctx, img, n, A, full=True, sampler=0, a0=0, a_count=None):
+    ctx.set_sampler(sampler)
+    tr = tt.TraceTransform(ctx, n, A, full=full, a0=a0, a_count=a_count)
+    out, med, rep = tr(img)
+    assert rep.ok()
+    return tr, out, med
+
+
+@pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
+@pytest.mark.parametrize("n,A,kind", SMALL)
+def test_fused_t05_bit_exact_vs_replay_and_within_tolerance_of_f64(ctx, n, A, kind, sampler):
+    img = tt.synth_image(kind, n)
+    tr, out, med = _run(ctx, img, n, A, sampler=sampler)
+    rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+    assert _bitwise_equal(out, rout), "GPU differs bitwise from the replay of its schedule"
+    assert np.array_equal(med, rmed)
+    fails, st = O.check(img, n, tr.ctab, tr.stab, tr.wtab, out, med)
+    assert fails == 0, st
+
+
+@pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
+@pytest.mark.parametrize("n,A,kind", [(64, 12, tt.DISK), (256, 360, tt.PHANTOM), (777, 5, tt.SPARSE),
+                                      (4096, 2, tt.DISK), (20000, 1, tt.DISK)])
+def test_radon_t0_bit_exact(ctx, n, A, kind, sampler):
+    img = tt.synth_image(kind, n)
+    tr, out, _ = _run(ctx, img, n, A, full=False, sampler=sampler)
+    rout, _, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY, full=False)
+    assert _bitwise_equal(out, rout)
+    fails, st = O.check(img, n, tr.ctab, tr.stab, tr.wtab, out, None, full=False)
+    assert fails == 0, st
+
+
+def test_radon_equals_t0_of_full_kernel(ctx):
+    n, A = 300, 17
+    img = tt.synth_image(tt.PHANTOM, n)
+    _, full, _ = _run(ctx, img, n, A)
+    _, t0, _ = _run(ctx, img, n, A, full=False)
+    assert _bitwise_equal(full[:, 0, :], t0[:, 0, :])
+
+
+def test_angle_shard_equals_slice_of_whole(ctx):
+    """Orientation sharding (a0, a_count) reproduces the unsharded slice exactly."""
+    n, A = 200, 24
+    img = tt.synth_image(tt.DISK, n)
+    _, whole, wmed = _run(ctx, img, n, A)
+    for a0, cnt in [(0, 6), (6, 6), (12, 11), (23, 1)]:
+        _, part, pmed = _run(ctx, img, n, A, a0=a0, a_count=cnt)
+        assert _bitwise_equal(part, whole[a0:a0 + cnt])
+        assert np.array_equal(pmed, wmed[a0:a0 + cnt])
+
+
+def test_zero_image_gives_zero_functionals_and_zero_medians(ctx):
+    n, A = 64, 6
+    img = np.zeros((n, n), np.float32)
+    _, out, med = _run(ctx, img, n, A)
+    assert not out.any() and not med.any()
+
+
+def test_constant_image_ties_are_accepted(ctx):
+    n, A = 128, 16
+    img = np.ones((n, n), np.float32)
+    tr, out, med = _run(ctx, img, n, A)
+    rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+    assert _bitwise_equal(out, rout) and np.array_equal(med, rmed)
+    fails, st = O.check(img, n, tr.ctab, tr.stab, tr.wtab, out, med)
+    assert fails == 0, st
+
+
+def test_random_dense_image_large_dynamic_range(ctx):
+    n, A = 257, 11
+    rng = np.random.default_rng(5)
+    img = (rng.random((n, n), dtype=np.float32) ** 4 * 1e3).astype(np.float32)
+    tr, out, med = _run(ctx, img, n, A)
+    rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+    assert _bitwise_equal(out, rout) and np.array_equal(med, rmed)
+    fails, st = O.check(img, n, tr.ctab, tr.stab, tr.wtab, out, med)
+    assert fails == 0, st
+
+
+def test_deterministic_across_launches(ctx):
+    n, A = 512, 30
+    img = tt.synth_image(tt.PHANTOM, n)
+    _, a, ma = _run(ctx, img, n, A)
+    _, b, mb = _run(ctx, img, n, A)
+    assert _bitwise_equal(a, b) and np.array_equal(ma, mb)
+
+
+@pytest.mark.slow
+def test_config2_full_size_1024_720(ctx):
+    """C2 (1024^2, 720 angles, T0-T5) at full size: bit-exact vs replay, tolerance vs f64."""
+    n, A = 1024, 720
+    img = tt.synth_image(tt.DISK, n)
+    tr, out, med = _run(ctx, img, n, A)
+    rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+    assert _bitwise_equal(out, rout) and np.array_equal(med, rmed)
+    fails, st = O.check(img, n, tr.ctab, tr.stab, tr.wtab, out, med)
+    assert fails == 0, st
+
+
+@pytest.mark.slow
+def test_config3_4096_1440_angle_subsample(ctx):
+    """C3 (4096^2, 1440 angles): full-size lines on a strided subset of angles."""
+    n, A = 4096, 1440
+    img = tt.synth_image(tt.DISK, n)
+    for a0 in (0, 181, 719, 1100):
+        tr, out, med = _run(ctx, img, n, A, a0=a0, a_count=2)
+        rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, a0=a0, a_count=2, mode=O.REPLAY)
+        assert _bitwise_equal(out, rout) and np.array_equal(med, rmed)
+        fails, st = O.check(img, n, tr.ctab, tr.stab, tr.wtab, out, med, a0=a0)
+        assert fails == 0, st
+
+
+def test_size_independent_properties_at_8192(ctx):
+    """Beyond oracle-friendly sizes: T0 of the angle pair (theta, theta+pi)
+    sums the same lines in opposite order, so T0(a, p) ~= T0(a+A/2, n-1-p);
+    the medians satisfy m + m(reversed) ~ n-1."""
+    n, A = 8192, 4
+    img = tt.synth_image(tt.DISK, n)
+    _, out, med = _run(ctx, img, n, A)
+    t0, t0r = out[0, 0].astype(np.float64), out[2, 0, ::-1].astype(np.float64)
+    mask = t0 > 1.0
+    assert mask.sum() > n // 2
+    assert np.max(np.abs(t0[mask] - t0r[mask]) / t0[mask]) < 1e-3
+    assert np.all(out[:, 1:] >= 0)
