@@ -173,7 +173,15 @@ def run_ours(args, ws, rank, local):
     n, A, full = wl["n"], wl["angles"], wl["full"]
     F = 6 if full else 1
     strong = args.workload == "c3" and ws > 1
-    a0, a_cnt = (rank * A // ws, (rank + 1) * A // ws - rank * A // ws) if strong else (0, A)
+    # Orientation shards keep the mirror pairing: rank r owns
+    # angles [a0, a0+cnt) and [A/2+a0, A/2+a0+cnt) -> rows [cnt] + [cnt].
+    h = A // 2
+    if strong:
+        from paper_1604_03410_b200 import shard
+        a0, cnt, pair = shard.orientation_shard(A, ws, rank)
+        a_cnt = 2 * cnt
+    else:
+        a0, a_cnt, pair = 0, A, 0
 
     stream = torch.cuda.Stream()
     sptr = stream.cuda_stream
@@ -186,6 +194,7 @@ def run_ours(args, ws, rank, local):
         med = torch.empty((a_cnt, 2, n), dtype=torch.int32, device="cuda")
         flush = torch.empty(int(256 << 20) // 4, device="cuda")  # > 126 MB L2
         gathered = torch.empty((A, F, n), device="cuda") if strong else None
+        gathered_raw = torch.empty((ws * a_cnt, F, n), device="cuda") if strong else None
         feats = torch.empty((ws, 2, F), device="cuda") if (ws > 1 and not strong) else None
     tex = None
     if args.sampler == 1:
@@ -194,14 +203,15 @@ def run_ours(args, ws, rank, local):
 
     def step():
         tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
-                        out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex)
+                        out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
+                        pair_stride=pair)
 
     def exchange():
         if not dist:
             return
         with torch.cuda.stream(stream):
-            if strong:  # the single NCCL gather of sinogram slices (equal shards: A % ws == 0)
-                dist.all_gather_into_tensor(gathered, out)
+            if strong:  # the single NCCL gather of sinogram slices (equal shards: (A/2) % ws == 0)
+                shard.gather_sinograms(out, A, dist, out=gathered, raw=gathered_raw)
             else:       # image-batch sharding: gather per-image feature summaries
                 f = torch.stack([out.sum(dim=(0, 2)), out.amax(dim=(0, 2))])
                 dist.all_gather_into_tensor(feats, f)
@@ -247,7 +257,8 @@ def run_ours(args, ws, rank, local):
     # ---- e2e through the public API (host buffers, copies in the timed region) ----
     ctx = tt.create_context(local)
     ctx.set_sampler(args.sampler)
-    tr = tt.TraceTransform(ctx, n, A, full=full, a0=a0, a_count=a_cnt)
+    # public API on this rank's share (contiguous angle block under torchrun c3)
+    tr = tt.TraceTransform(ctx, n, A, full=full, a0=rank * a_cnt if strong else 0, a_count=a_cnt)
     from paper_1604_03410_b200._lib import lib
     import ctypes as C
     nb_img, nb_out, nb_med = n * n * 4, a_cnt * F * n * 4, a_cnt * 2 * n * 4
@@ -275,14 +286,16 @@ def run_ours(args, ws, rank, local):
            "d2h_bytes_per_step": nb_out + (nb_med if full else 0), "ms_per_step": e2e_s * 1e3,
            "api": "TraceTransform.run_resident -> tt_memcpy_htod / tt_launch(trace_t05) / tt_memcpy_dtoh"}
     # parity spot check of the e2e output against the device-resident one
-    same = np.array_equal(h_out.reshape(a_cnt, F, n), out.cpu().numpy())
+    same = (not strong) and np.array_equal(h_out.reshape(a_cnt, F, n), out.cpu().numpy())
     tr.free_resident()
     ctx.destroy()
     for h in hp:
         lib.tt_host_free(h)
 
     # ---- roofline of the fused kernel (rank 0's shard) ----
-    taps = lib.tt_count_inbounds_taps(n, a0, a_cnt, ctab_h.ctypes.data, stab_h.ctypes.data)
+    taps = lib.tt_count_inbounds_taps(n, a0, a_cnt // 2, ctab_h.ctypes.data, stab_h.ctypes.data) + \
+        lib.tt_count_inbounds_taps(n, a0 + h, a_cnt // 2, ctab_h.ctypes.data, stab_h.ctypes.data) if strong else \
+        lib.tt_count_inbounds_taps(n, 0, A, ctab_h.ctypes.data, stab_h.ctypes.data)
     kern_s = statistics.mean(kern_ms) / 1e3
     peak = fp32_peak_tflops(torch, tt, stream)
     achieved = FLOPS_PER_TAP[full] * taps / kern_s / 1e12

@@ -196,7 +196,8 @@ tt_status tt_counters_json(tt_ctx* ctx, char* buf, size_t cap, size_t* needed);
 tt_status tt_events(tt_ctx* ctx, uint8_t* buf, size_t cap, size_t* needed);
 
 /* ---- trace-transform helpers (spec DESIGN.md §2) ------------------------------------ */
-/* Host tables: ctab/stab[a_total], wtab[6*n] (any may be NULL). */
+/* Host tables: ctab/stab[a_total], wtab[8*n] = per r: r, r^2, w3re, w3im,
+ * w4re, w4im, w5re, w5im (any may be NULL). */
 tt_status tt_make_tables(int n, int a_total, float* ctab, float* stab, float* wtab);
 /* Deterministic synthetic images: kind 0 disk-noise, 1 phantom, 2 sparse. */
 tt_status tt_synth_image(int kind, uint64_t seed, int n, float* img);
@@ -216,10 +217,14 @@ uint64_t tt_count_inbounds_taps(int n, int a0, int a_count, const float* ctab, c
 tt_status tt_ffma_probe(float* d_out, int blocks, int iters, void* stream);
 
 /* Raw device-pointer entry (multi-GPU driver, benchmarks): enqueue the fused
- * kernel for angles [a0, a0+a_count) on `stream` (cudaStream_t; NULL = legacy
+ * kernel for a_count angles on `stream` (cudaStream_t; NULL = legacy
  * default).  out: full ? [a_count][6][n] : [a_count][n]; med may be NULL.
  * sampler: 0 = global/L1 loads, 1 = texture gather (a cudaArray copy of img
- * is made and released by this call). */
+ * is made and released by this call).
+ * pair_stride: 0 = the drop-in rule (angles [a0, a0+a_count); pairs
+ * (a0+i, a0+i+a_count/2) when a_count is even); -1 = no pairing; > 0 = the
+ * angles are a0+i and a0+i+pair_stride for i < a_count/2 (rows i and
+ * a_count/2+i) — an orientation shard together with its mirror half. */
 typedef struct tt_trace_desc {
     const float* img;
     int32_t n;
@@ -232,7 +237,7 @@ typedef struct tt_trace_desc {
     float* out;
     int32_t* med;
     int32_t sampler;
-    int32_t _pad;
+    int32_t pair_stride;
 } tt_trace_desc;
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
 

@@ -53,6 +53,8 @@ def lib():
         L.tto_schedule_warps.restype = ctypes.c_int
         L.tto_transform.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, ip, dp, dp, ctypes.c_int]
+        L.tto_replay_launch.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
+                                        ctypes.c_int, ctypes.c_int, fp, ip, ctypes.c_int]
         L.tto_line_f64.argtypes = [fp, ctypes.c_int, fp, ctypes.c_int, ctypes.c_int, dp, dp, ip]
         L.tto_check.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
                                 ctypes.c_int, fp, ip, ctypes.c_double, ctypes.c_int, ctypes.c_double, dp, ctypes.c_int]
@@ -72,7 +74,7 @@ def _f(a):
 def tables(n: int, a_total: int):
     c = np.empty(a_total, np.float32)
     s = np.empty(a_total, np.float32)
-    w = np.empty(6 * n, np.float32)
+    w = np.empty(8 * n, np.float32)
     lib().tto_tables(n, a_total, _f(c), _f(s), _f(w))
     return c, s, w
 
@@ -107,6 +109,18 @@ def transform(img, n, ctab, stab, wtab, *, a0=0, a_count=None, full=True, mode=F
                         _f(wtab), int(full), mode, W, _f(out), _p(med, ctypes.c_int32),
                         _p(out64, ctypes.c_double), _p(absm, ctypes.c_double), nthreads)
     return out, med, out64, absm
+
+
+def replay_launch(img, n, ctab, stab, wtab, *, a0, units, pair_stride, full=True, W=0, nthreads=0):
+    """Replay of one raw B200 launch (tt_trace_device with explicit structure).
+    Returns (out [rows][F][n], med [rows][2][n]) with rows = units * (2 if pair_stride else 1)."""
+    rows = units * (2 if pair_stride > 0 else 1)
+    F = NF if full else 1
+    out = np.zeros((rows, F, n), np.float32)
+    med = np.zeros((rows, 2, n), np.int32)
+    lib().tto_replay_launch(_f(np.ascontiguousarray(img, np.float32)), n, a0, units, pair_stride, _f(ctab),
+                            _f(stab), _f(wtab), int(full), W, _f(out), _p(med, ctypes.c_int32), nthreads)
+    return out, (med if full else None)
 
 
 def check(img, n, ctab, stab, wtab, gpu_out, gpu_med=None, *, a0=0, full=True, rtol=1e-4, W=0, chain=0.0,

@@ -8,7 +8,7 @@
 //
 // Usage: tt_tier2 <in.bin> <out.bin> <a0> <a_count> <threads> [krn] [lines]
 //   lines: only lines p < lines are launched (bounded benchmark samples)
-//   in.bin : int32 n, int32 A, then f32 img[n*n], ctab[A], stab[A], wtab[6n]
+//   in.bin : int32 n, int32 A, then f32 img[n*n], ctab[A], stab[A], wtab[8n]
 //   out.bin: f32 out[a_count][6][n], int32 med[a_count][2][n]
 //   stdout : one JSON line {"taps":..., "seconds":..., "threads":...}
 //
@@ -63,7 +63,7 @@ int main(int argc, char** argv) {
     std::memcpy(&n, q, 4);
     std::memcpy(&A, q + 4, 4);
     q += 8;
-    std::vector<float> img(size_t(n) * n), ctab(A), stab(A), wtab(size_t(6) * n);
+    std::vector<float> img(size_t(n) * n), ctab(A), stab(A), wtab(size_t(8) * n);
     std::memcpy(img.data(), q, img.size() * 4);
     q += img.size() * 4;
     std::memcpy(ctab.data(), q, ctab.size() * 4);

@@ -23,6 +23,9 @@
 
 /* ---------------------------------------------------------------- tables */
 
+/* wtab layout [n][8] per r: r, r^2, w3re, w3im, w4re, w4im, w5re, w5im */
+#define WT(w, r, j) ((w)[8 * (size_t)(r) + 2 + (j)])
+
 /* spec §2.1: theta_a = 2*pi*a/A evaluated in f64, rounded to f32 once. */
 void tto_tables(int n, int a_total, float* ctab, float* stab, float* wtab) {
     const double two_pi = 6.283185307179586476925286766559;
@@ -42,12 +45,12 @@ void tto_tables(int n, int a_total, float* ctab, float* stab, float* wtab) {
             w4r = cos(3.0 * lr);      w4i = sin(3.0 * lr);
             w5r = sr * cos(4.0 * lr); w5i = sr * sin(4.0 * lr);
         }
-        wtab[0 * (size_t)n + r] = (float)w3r;
-        wtab[1 * (size_t)n + r] = (float)w3i;
-        wtab[2 * (size_t)n + r] = (float)w4r;
-        wtab[3 * (size_t)n + r] = (float)w4i;
-        wtab[4 * (size_t)n + r] = (float)w5r;
-        wtab[5 * (size_t)n + r] = (float)w5i;
+        float* e = wtab + 8 * (size_t)r;
+        e[0] = (float)r;
+        e[1] = (float)((double)r * (double)r);
+        e[2] = (float)w3r; e[3] = (float)w3i;
+        e[4] = (float)w4r; e[5] = (float)w4i;
+        e[6] = (float)w5r; e[7] = (float)w5i;
     }
 }
 
@@ -171,8 +174,6 @@ void tto_line_f64(const float* v, int n, const float* wtab, int m_force, int mp_
     int mp = (Sp > 0.0) ? median64(sv, n, Sp) : 0;
     if (m_force >= 0) m = m_force;
     if (mp_force >= 0) mp = mp_force;
-    const float *w3r = wtab, *w3i = wtab + n, *w4r = wtab + 2 * (size_t)n, *w4i = wtab + 3 * (size_t)n,
-                *w5r = wtab + 4 * (size_t)n, *w5i = wtab + 5 * (size_t)n;
     double t1 = 0, t2 = 0, a3r = 0, a3i = 0, a4r = 0, a4i = 0, a5r = 0, a5i = 0;
     double m3 = 0, m4 = 0, m5 = 0;
     for (int t = m; t < n; ++t) {
@@ -180,16 +181,16 @@ void tto_line_f64(const float* v, int n, const float* wtab, int m_force, int mp_
         double vv = (double)v[t];
         t1 += (double)r * vv;
         t2 += (double)r * (double)r * vv;
-        a3r += (double)w3r[r] * vv; a3i += (double)w3i[r] * vv;
-        a4r += (double)w4r[r] * vv; a4i += (double)w4i[r] * vv;
-        m3 += (fabs((double)w3r[r]) + fabs((double)w3i[r])) * vv;
-        m4 += (fabs((double)w4r[r]) + fabs((double)w4i[r])) * vv;
+        a3r += (double)WT(wtab, r, 0) * vv; a3i += (double)WT(wtab, r, 1) * vv;
+        a4r += (double)WT(wtab, r, 2) * vv; a4i += (double)WT(wtab, r, 3) * vv;
+        m3 += (fabs((double)WT(wtab, r, 0)) + fabs((double)WT(wtab, r, 1))) * vv;
+        m4 += (fabs((double)WT(wtab, r, 2)) + fabs((double)WT(wtab, r, 3))) * vv;
     }
     for (int t = mp; t < n; ++t) {
         int r = t - mp;
         double vv = (double)sv[t];
-        a5r += (double)w5r[r] * vv; a5i += (double)w5i[r] * vv;
-        m5 += (fabs((double)w5r[r]) + fabs((double)w5i[r])) * vv;
+        a5r += (double)WT(wtab, r, 4) * vv; a5i += (double)WT(wtab, r, 5) * vv;
+        m5 += (fabs((double)WT(wtab, r, 4)) + fabs((double)WT(wtab, r, 5))) * vv;
     }
     out[0] = S; out[1] = t1; out[2] = t2;
     out[3] = sqrt(a3r * a3r + a3i * a3i);
@@ -222,21 +223,19 @@ static void line_seq32(const float* v, float* sv, int n, const float* wtab, floa
     }
     int m = median32_seq(v, n, S);
     int mp = median32_seq(sv, n, Sp);
-    const float *w3r = wtab, *w3i = wtab + n, *w4r = wtab + 2 * (size_t)n, *w4i = wtab + 3 * (size_t)n,
-                *w5r = wtab + 4 * (size_t)n, *w5i = wtab + 5 * (size_t)n;
     float a1 = 0, a2 = 0, a3r = 0, a3i = 0, a4r = 0, a4i = 0, a5r = 0, a5i = 0;
     for (int t = m; t < n; ++t) {
         int r = t - m;
         float rf = (float)r, r2 = rf * rf, vv = v[t];
         a1 = fmaf(rf, vv, a1);
         a2 = fmaf(r2, vv, a2);
-        a3r = fmaf(w3r[r], vv, a3r); a3i = fmaf(w3i[r], vv, a3i);
-        a4r = fmaf(w4r[r], vv, a4r); a4i = fmaf(w4i[r], vv, a4i);
+        a3r = fmaf(WT(wtab, r, 0), vv, a3r); a3i = fmaf(WT(wtab, r, 1), vv, a3i);
+        a4r = fmaf(WT(wtab, r, 2), vv, a4r); a4i = fmaf(WT(wtab, r, 3), vv, a4i);
     }
     for (int t = mp; t < n; ++t) {
         int r = t - mp;
         float vv = sv[t];
-        a5r = fmaf(w5r[r], vv, a5r); a5i = fmaf(w5i[r], vv, a5i);
+        a5r = fmaf(WT(wtab, r, 4), vv, a5r); a5i = fmaf(WT(wtab, r, 5), vv, a5i);
     }
     out[0] = S; out[1] = a1; out[2] = a2;
     out[3] = sqrtf(fmaf(a3r, a3r, a3i * a3i));
@@ -284,7 +283,27 @@ static float replay_strided_sum(const float* v, int len, int W) {
     return total;
 }
 
-static int replay_median(const float* v, int n, float S, int W) {
+/* Cooperative rescan of the crossing chunk (kernel: one warp, 32 elements
+ * per block, Kogge-Stone scan per block, ballot for the first crossing). */
+static int replay_rescan(const float* u, int n, int start, int K, float exc, float S) {
+    int len = n - start;
+    if (len > K) len = K;
+    float C = 0.0f;
+    for (int b = 0; b * 32 < len; ++b) {
+        float x[32];
+        for (int j = 0; j < 32; ++j) x[j] = (b * 32 + j < len) ? u[start + b * 32 + j] : 0.0f;
+        warp_scan(x);
+        for (int j = 0; j < 32 && b * 32 + j < len; ++j) {
+            float P = exc + (C + x[j]);
+            if (P + P >= S) return start + b * 32 + j;
+        }
+        C = C + x[31];
+    }
+    return len > 0 ? start + len - 1 : n - 1;
+}
+
+/* Weighted median of u under the kernel's schedule. */
+static int replay_median(const float* u, int n, float S, int W) {
     const int nslot = 32 * W;
     const int K = (n + nslot - 1) / nslot;
     float E = 0.0f;
@@ -293,48 +312,30 @@ static int replay_median(const float* v, int n, float S, int W) {
         for (int l = 0; l < 32; ++l) {
             int k = 32 * w + l;
             float acc = 0.0f;
-            for (int t = k * K; t < n && t < (k + 1) * K; ++t) acc = acc + v[t];
+            for (int t = k * K; t < n && t < (k + 1) * K; ++t) acc = acc + u[t];
             c[l] = acc;
             inc[l] = acc;
         }
         warp_scan(inc);
         for (int l = 0; l < 32; ++l) {
-            int k = 32 * w + l;
             float e = (l == 0) ? 0.0f : inc[l - 1];
             float exc = E + e;
             float pend = exc + c[l];
-            if (pend + pend >= S) {
-                /* first qualifying slot: rescan its chunk */
-                float q = 0.0f;
-                int last = k * K;
-                for (int t = k * K; t < n && t < (k + 1) * K; ++t) {
-                    q = q + v[t];
-                    float P = exc + q;
-                    last = t;
-                    if (P + P >= S) return t;
-                }
-                return last < n ? last : n - 1;
-            }
+            if (pend + pend >= S) return replay_rescan(u, n, (32 * w + l) * K, K, exc, S);
         }
         E = E + inc[31];
     }
     return 0;
 }
 
-static void line_replay(const float* v, float* sv, int n, const float* wtab, int W, int full, float out[6],
-                        int32_t med[2]) {
-    if (full)
-        for (int t = 0; t < n; ++t) sv[t] = sqrtf(v[t]);
-    float S = replay_strided_sum(v, n, W);
-    out[0] = S;
-    if (!full) return;
-    float Sp = replay_strided_sum(sv, n, W);
-    int m = replay_median(v, n, S, W);
-    int mp = replay_median(sv, n, Sp, W);
+/* Medians + pass 2 for one line direction u (su = sqrt u) with the line's
+ * S, S' (shared by both directions of a mirrored pair). */
+static void replay_emit(const float* u, const float* su, int n, const float* wtab, int W, float S, float Sp,
+                        float out[6], int32_t med[2]) {
+    int m = replay_median(u, n, S, W);
+    int mp = replay_median(su, n, Sp, W);
     const int R = n - m, Rp = n - mp, Rmax = R > Rp ? R : Rp;
     const int nslot = 32 * W;
-    const float *w3r = wtab, *w3i = wtab + n, *w4r = wtab + 2 * (size_t)n, *w4i = wtab + 3 * (size_t)n,
-                *w5r = wtab + 4 * (size_t)n, *w5i = wtab + 5 * (size_t)n;
     float tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int w = 0; w < W; ++w) {
         float x[8][32];
@@ -342,21 +343,22 @@ static void line_replay(const float* v, float* sv, int n, const float* wtab, int
             float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int r = 32 * w + l; r < Rmax; r += nslot) {
                 float rf = (float)r, r2 = rf * rf;
-                float vv = (r < R) ? v[m + r] : 0.0f;
-                float ss = (r < Rp) ? sv[mp + r] : 0.0f;
+                float vv = (r < R) ? u[m + r] : 0.0f;
+                float ss = (r < Rp) ? su[mp + r] : 0.0f;
                 a[0] = fmaf(rf, vv, a[0]);
                 a[1] = fmaf(r2, vv, a[1]);
-                a[2] = fmaf(w3r[r], vv, a[2]);
-                a[3] = fmaf(w3i[r], vv, a[3]);
-                a[4] = fmaf(w4r[r], vv, a[4]);
-                a[5] = fmaf(w4i[r], vv, a[5]);
-                a[6] = fmaf(w5r[r], ss, a[6]);
-                a[7] = fmaf(w5i[r], ss, a[7]);
+                a[2] = fmaf(WT(wtab, r, 0), vv, a[2]);
+                a[3] = fmaf(WT(wtab, r, 1), vv, a[3]);
+                a[4] = fmaf(WT(wtab, r, 2), vv, a[4]);
+                a[5] = fmaf(WT(wtab, r, 3), vv, a[5]);
+                a[6] = fmaf(WT(wtab, r, 4), ss, a[6]);
+                a[7] = fmaf(WT(wtab, r, 5), ss, a[7]);
             }
             for (int j = 0; j < 8; ++j) x[j][l] = a[j];
         }
         for (int j = 0; j < 8; ++j) tot[j] = tot[j] + warp_butterfly(x[j]);
     }
+    out[0] = S;
     out[1] = tot[0];
     out[2] = tot[1];
     out[3] = sqrtf(fmaf(tot[2], tot[2], tot[3] * tot[3]));
@@ -364,6 +366,85 @@ static void line_replay(const float* v, float* sv, int n, const float* wtab, int
     out[5] = sqrtf(fmaf(tot[6], tot[6], tot[7] * tot[7]));
     med[0] = m;
     med[1] = mp;
+}
+
+static int mirrored(const float* ctab, const float* stab, int a, int ap) {
+    float mc = -ctab[a], ms = -stab[a];
+    return memcmp(&mc, &ctab[ap], 4) == 0 && memcmp(&ms, &stab[ap], 4) == 0;
+}
+
+static void put(float* out, int32_t* med, int F, int n, int row, int col, const float o[6], const int32_t md[2]) {
+    for (int f = 0; f < F; ++f) out[((size_t)row * F + f) * n + col] = o[f];
+    if (med && F == TTO_NF) {
+        med[((size_t)row * 2 + 0) * n + col] = md[0];
+        med[((size_t)row * 2 + 1) * n + col] = md[1];
+    }
+}
+
+/* One launch unit of the kernel: line (a0+i, p) and, with pairing, its
+ * partner angle a0+i+pair_stride (the mirrored line n-1-p of the same
+ * samples when the tables are exactly mirrored, else sampled separately). */
+static void replay_unit(const float* img, int n, int a0, int units, int pair_stride, const float* ctab,
+                        const float* stab, const float* wtab, int full, int W, int i, int p, float* v, float* sv,
+                        float* rv, float* rsv, float* out, int32_t* med) {
+    const int F = full ? TTO_NF : 1;
+    const int nlines = (pair_stride > 0) ? 2 : 1;
+    const int mir = (pair_stride > 0) && mirrored(ctab, stab, a0 + i, a0 + i + pair_stride);
+    for (int li = 0; li < (mir ? 1 : nlines); ++li) {
+        const int a = a0 + i + li * pair_stride;
+        if (n >= 2) tto_line_samples(img, n, ctab[a], stab[a], p, v);
+        else for (int t = 0; t < n; ++t) v[t] = 0.0f;
+        for (int t = 0; t < n; ++t) sv[t] = sqrtf(v[t]);
+        const float S = replay_strided_sum(v, n, W);
+        const float Sp = replay_strided_sum(sv, n, W);
+        float o[6] = {S, 0, 0, 0, 0, 0};
+        int32_t md[2] = {0, 0};
+        if (full) replay_emit(v, sv, n, wtab, W, S, Sp, o, md);
+        put(out, med, F, n, i + li * units, p, o, md);
+        if (mir) {
+            for (int t = 0; t < n; ++t) {
+                rv[t] = v[n - 1 - t];
+                rsv[t] = sv[n - 1 - t];
+            }
+            float o2[6] = {S, 0, 0, 0, 0, 0};
+            int32_t md2[2] = {0, 0};
+            if (full) replay_emit(rv, rsv, n, wtab, W, S, Sp, o2, md2);
+            put(out, med, F, n, i + units, n - 1 - p, o2, md2);
+        }
+    }
+}
+
+void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stride, const float* ctab,
+                       const float* stab, const float* wtab, int full, int W, float* out, int32_t* med,
+                       int nthreads) {
+    if (W <= 0) W = tto_schedule_warps(n);
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    const long total = (long)units * n;
+#pragma omp parallel
+    {
+        float* buf = (float*)malloc(sizeof(float) * 4 * (size_t)(n > 0 ? n : 1));
+#pragma omp for schedule(dynamic, 64)
+        for (long L = 0; L < total; ++L)
+            replay_unit(img, n, a0, units, pair_stride, ctab, stab, wtab, full, W, (int)(L / n), (int)(L % n), buf,
+                        buf + n, buf + 2 * (size_t)n, buf + 3 * (size_t)n, out, med);
+        free(buf);
+    }
+}
+
+/* The structure the native trace_t05 / radon launcher uses for a launch of
+ * a_count angles from a0: pairs (a0+i, a0+i+a_count/2) when a_count is even. */
+void tto_launch_structure(int a_count, int* units, int* pair_stride) {
+    if (a_count >= 2 && a_count % 2 == 0) {
+        *units = a_count / 2;
+        *pair_stride = a_count / 2;
+    } else {
+        *units = a_count;
+        *pair_stride = 0;
+    }
 }
 
 /* ------------------------------------------------------------- transform */
@@ -374,6 +455,12 @@ void tto_transform(const float* img, int n, int a0, int a_count, int a_total, co
     (void)a_total;
     const int F = full ? TTO_NF : 1;
     if (W <= 0) W = tto_schedule_warps(n);
+    if (mode == TTO_REPLAY) {
+        int units, stride;
+        tto_launch_structure(a_count, &units, &stride);
+        tto_replay_launch(img, n, a0, units, stride, ctab, stab, wtab, full, W, out, med, nthreads);
+        return;
+    }
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #else
@@ -414,7 +501,7 @@ void tto_transform(const float* img, int n, int a0, int a_count, int a_total, co
                     o32[0] = S;
                 }
             } else {
-                line_replay(v, sv, n, wtab, W, full, o32, md);
+                /* REPLAY is dispatched before this loop (launch-unit structure) */
             }
             for (int f = 0; f < F; ++f) out[((size_t)ai * F + f) * n + p] = o32[f];
             if (med && full) {

@@ -47,7 +47,7 @@ enum { TTO_DISK = 0, TTO_PHANTOM = 1, TTO_SPARSE = 2 };
 #define TTO_NF 6
 
 /* Host tables (spec §2.1/§2.2): ctab/stab[A] = (float)cos/sin(2*pi*a/A) in
- * f64; wtab planar [6][n] = w3re,w3im,w4re,w4im,w5re,w5im (f64 -> f32). */
+ * f64; wtab [n][8] = r, r^2, w3re, w3im, w4re, w4im, w5re, w5im (f64 -> f32). */
 void tto_tables(int n, int a_total, float* ctab, float* stab, float* wtab);
 
 /* Deterministic synthetic images (spec §2.4). */
@@ -72,6 +72,18 @@ void tto_transform(const float* img, int n, int a0, int a_count, int a_total,
                    const float* ctab, const float* stab, const float* wtab,
                    int full, int mode, int W, float* out, int32_t* med,
                    double* out64, double* absm, int nthreads);
+
+/* Replay of one B200 launch: units (a0+i, p), i < units;
+ * with pair_stride > 0 each unit also owns angle a0+i+pair_stride (rows
+ * units+i), processed as the mirrored line n-1-p of the same samples when
+ * ctab/stab are exactly mirrored, else sampled separately. */
+void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stride, const float* ctab,
+                       const float* stab, const float* wtab, int full, int W, float* out, int32_t* med,
+                       int nthreads);
+
+/* Launch structure the native trace_t05/radon launcher uses for a_count
+ * angles: pairs (i, i + a_count/2) when a_count is even. */
+void tto_launch_structure(int a_count, int* units, int* pair_stride);
 
 /* Per-line truth evaluated at forced medians (tie re-evaluation, §2.5).
  * m_force / mp_force < 0 -> use the f64 medians. */

@@ -51,7 +51,7 @@ class Counters(C.Structure):
 class TraceDesc(C.Structure):
     _fields_ = [("img", C.c_void_p), ("n", C.c_int32), ("a0", C.c_int32), ("a_count", C.c_int32),
                 ("full", C.c_int32), ("ctab", C.c_void_p), ("stab", C.c_void_p), ("wtab", C.c_void_p),
-                ("out", C.c_void_p), ("med", C.c_void_p), ("sampler", C.c_int32), ("_pad", C.c_int32)]
+                ("out", C.c_void_p), ("med", C.c_void_p), ("sampler", C.c_int32), ("pair_stride", C.c_int32)]
 
 
 ARG_I32, ARG_I64, ARG_F32, ARG_F64, ARG_PTR = range(5)

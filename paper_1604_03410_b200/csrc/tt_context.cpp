@@ -56,6 +56,7 @@ struct Param {
     bool ptr = false;
     Scalar type = Scalar::I32;
     std::string name;
+    bool written = false;  // the native kernel stores through this pointer
     bool operator==(const Param& o) const { return ptr == o.ptr && type == o.type; }
     std::string type_text() const { return ptr ? std::string("ptr.global.") + scalar_name(type) : scalar_name(type); }
     std::string sig_text() const { return ptr ? std::string(scalar_name(type)) + "[]" : scalar_name(type); }
@@ -79,6 +80,8 @@ struct ResolvedArg {
     tt_arg value;          // scalars
     void* dptr = nullptr;  // device address for pointers
     std::uint64_t bytes = 0;
+    std::uint64_t base = 0;  // synthetic address (allocation key)
+    std::uint64_t gen = 0;   // write generation of the allocation
 };
 
 struct LaunchOutcome {
@@ -102,6 +105,16 @@ struct Alloc {
     void* dptr = nullptr;
     std::uint64_t bytes = 0;
     bool live = true;
+    std::uint64_t gen = 0;  // bumped by every write (H2D copy, written launch argument)
+};
+
+// Texture-gather sampler state cached per image allocation: the block-linear
+// cudaArray copy is refreshed only when the allocation's generation changed.
+struct TexEntry {
+    std::uint64_t gen = ~0ull;
+    int n = 0;
+    cudaArray_t arr = nullptr;
+    cudaTextureObject_t tex = 0;
 };
 
 struct LaunchRecord {
@@ -148,9 +161,19 @@ struct tt_ctx {
     std::uint64_t h2d_mark = 0, d2h_mark = 0;
 
     std::string last_error;
+    std::map<std::uint64_t, TexEntry> tex_cache;  // keyed by image allocation base
 };
 
 namespace {
+
+void drop_texture(tt_ctx* ctx, std::uint64_t base) {
+    auto it = ctx->tex_cache.find(base);
+    if (it == ctx->tex_cache.end()) return;
+    cudaStreamSynchronize(ctx->stream);
+    cudaDestroyTextureObject(it->second.tex);
+    cudaFreeArray(it->second.arr);
+    ctx->tex_cache.erase(it);
+}
 
 tt_status fail(const tt_ctx* ctx, tt_status st, const std::string& msg) {
     if (ctx) const_cast<tt_ctx*>(ctx)->last_error = msg;
@@ -454,7 +477,7 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     const std::int64_t F = full ? tt::kNumF : 1;
     bool oob = a0 < 0 || elems(img, 4) < N * N || std::int64_t(elems(ct, 4)) < a0 + a_count ||
                std::int64_t(elems(st, 4)) < a0 + a_count || elems(out, 4) < std::uint64_t(a_count * F) * N;
-    if (wt) oob = oob || elems(*wt, 4) < 6 * N;
+    if (wt) oob = oob || elems(*wt, 4) < 8 * N;
     if (med) oob = oob || elems(*med, 4) < std::uint64_t(a_count) * 2 * N;
     if (oob) {
         o.trap = first_thread_trap(TT_TRAP_GLOBAL_OUT_OF_BOUNDS);
@@ -464,7 +487,7 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     ta.img = (const float*)img.dptr;
     ta.n = n;
     ta.a0 = a0;
-    ta.a_count = int(a_count);
+    tt::launch_structure(int(a_count), &ta.a_count, &ta.pair_stride);
     ta.ctab = (const float*)ct.dptr;
     ta.stab = (const float*)st.dptr;
     ta.wtab = wt ? (const float*)wt->dptr : nullptr;
@@ -472,18 +495,32 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     ta.med = med ? (std::int32_t*)med->dptr : nullptr;
     ta.full = full;
     ta.sampler = tt::Sampler(ctx.sampler);
-    cudaArray_t arr = nullptr;
     if (ta.sampler == tt::Sampler::Texture) {
-        cudaError_t e = tt::make_image_texture(ta.img, n, ctx.stream, &arr, &ta.tex);
-        if (e != cudaSuccess) return cuda_outcome(e, "make_image_texture");
+        TexEntry& te = ctx.tex_cache[img.base];
+        if (te.arr == nullptr || te.n != n) {
+            if (te.arr) {
+                cudaStreamSynchronize(ctx.stream);
+                cudaDestroyTextureObject(te.tex);
+                cudaFreeArray(te.arr);
+                te = TexEntry{};
+            }
+            cudaError_t e = tt::make_image_texture(ta.img, n, ctx.stream, &te.arr, &te.tex);
+            if (e != cudaSuccess) {
+                ctx.tex_cache.erase(img.base);
+                return cuda_outcome(e, "make_image_texture");
+            }
+            te.n = n;
+            te.gen = img.gen;
+        } else if (te.gen != img.gen) {  // image rewritten since the copy: refresh (stream-ordered)
+            cudaError_t e = cudaMemcpy2DToArrayAsync(te.arr, 0, 0, ta.img, std::size_t(n) * 4, std::size_t(n) * 4,
+                                                     std::size_t(n), cudaMemcpyDeviceToDevice, ctx.stream);
+            if (e != cudaSuccess) return cuda_outcome(e, "texture refresh");
+            te.gen = img.gen;
+        }
+        ta.tex = te.tex;
     }
     o = cuda_outcome(tt::launch_trace(ta, ctx.stream), "trace kernel");
     o.gpu_launches = tt::trace_launch_count(ta);
-    if (arr) {
-        cudaStreamSynchronize(ctx.stream);
-        cudaDestroyTextureObject(ta.tex);
-        cudaFreeArray(arr);
-    }
     return o;
 }
 
@@ -499,11 +536,12 @@ LaunchOutcome run_radon(tt_ctx& ctx, const tt_grid& g, const std::vector<Resolve
     return run_trace_common(ctx, g, a[0], a[1].value.v.i32, a[2], a[3], nullptr, a[4], nullptr, a[5].value.v.i32, false);
 }
 
-Param P(bool ptr, Scalar t, const char* name) {
+Param P(bool ptr, Scalar t, const char* name, bool written = false) {
     Param p;
     p.ptr = ptr;
     p.type = t;
     p.name = name;
+    p.written = written;
     return p;
 }
 
@@ -520,19 +558,19 @@ const std::vector<NativeKernel>& registry() {
         const Scalar f = Scalar::F32, d = Scalar::F64, i = Scalar::I32, l = Scalar::I64;
         add("trace_t05",
             {P(true, f, "img"), P(false, i, "n"), P(true, f, "ctab"), P(true, f, "stab"), P(true, f, "wtab"),
-             P(true, f, "out"), P(true, i, "med"), P(false, i, "a0")},
+             P(true, f, "out", true), P(true, i, "med", true), P(false, i, "a0")},
             run_trace_t05);
         add("radon",
-            {P(true, f, "img"), P(false, i, "n"), P(true, f, "ctab"), P(true, f, "stab"), P(true, f, "out"),
+            {P(true, f, "img"), P(false, i, "n"), P(true, f, "ctab"), P(true, f, "stab"), P(true, f, "out", true),
              P(false, i, "a0")},
             run_radon);
-        add("vadd", {P(true, f, "a"), P(true, f, "b"), P(true, f, "c")}, run_vadd<tt::ElemKind::F32, 4>);
-        add("vadd", {P(true, d, "a"), P(true, d, "b"), P(true, d, "c")}, run_vadd<tt::ElemKind::F64, 8>);
-        add("vadd", {P(true, i, "a"), P(true, i, "b"), P(true, i, "c")}, run_vadd<tt::ElemKind::I32, 4>);
-        add("vadd", {P(true, l, "a"), P(true, l, "b"), P(true, l, "c")}, run_vadd<tt::ElemKind::I64, 8>);
-        add("scale", {P(true, f, "a"), P(false, f, "k")}, run_scale);
-        add("copy", {P(true, f, "a"), P(true, f, "b")}, run_copy);
-        add("add_to", {P(true, f, "inp"), P(true, f, "out")}, run_add_to);
+        add("vadd", {P(true, f, "a"), P(true, f, "b"), P(true, f, "c", true)}, run_vadd<tt::ElemKind::F32, 4>);
+        add("vadd", {P(true, d, "a"), P(true, d, "b"), P(true, d, "c", true)}, run_vadd<tt::ElemKind::F64, 8>);
+        add("vadd", {P(true, i, "a"), P(true, i, "b"), P(true, i, "c", true)}, run_vadd<tt::ElemKind::I32, 4>);
+        add("vadd", {P(true, l, "a"), P(true, l, "b"), P(true, l, "c", true)}, run_vadd<tt::ElemKind::I64, 8>);
+        add("scale", {P(true, f, "a", true), P(false, f, "k")}, run_scale);
+        add("copy", {P(true, f, "a"), P(true, f, "b", true)}, run_copy);
+        add("add_to", {P(true, f, "inp"), P(true, f, "out", true)}, run_add_to);
         return r;
     }();
     return reg;
@@ -620,6 +658,7 @@ tt_status tt_ctx_destroy(tt_ctx* ctx) {
     TT_CHECK_CTX(ctx);
     DeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    while (!ctx->tex_cache.empty()) drop_texture(ctx, ctx->tex_cache.begin()->first);
     for (auto& kv : ctx->allocs)
         if (kv.second.live && kv.second.dptr) cudaFreeAsync(kv.second.dptr, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
@@ -751,6 +790,7 @@ tt_status tt_mem_free(tt_ctx* ctx, tt_devptr p) {
     if (it == ctx->allocs.end() || !it->second.live)
         return fail(ctx, TT_ERR_DOUBLE_FREE, "DoubleFree: device pointer already freed");
     DeviceGuard guard(ctx->device);
+    drop_texture(ctx, p.base);
     cudaError_t e = cudaFreeAsync(it->second.dptr, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFreeAsync");
     it->second.live = false;  // the address stays reserved: never reused
@@ -775,6 +815,7 @@ tt_status tt_memcpy_htod(tt_ctx* ctx, tt_devptr dst, const void* src, std::uint6
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // synchronous like driver.hpp:195
         if (e != cudaSuccess) return cuda_fail(ctx, e, "memcpy_htod");
     }
+    ++a->gen;
     ctx->c.bytes_h2d += bytes;
     ctx->events.push_back(TT_EV_H2D);
     return TT_OK;
@@ -806,6 +847,7 @@ tt_status tt_mem_device_pointer(tt_ctx* ctx, tt_devptr p, void** out) {
     Alloc* a = nullptr;
     tt_status st = lookup(ctx, p, &a);
     if (st != TT_OK) return st;
+    ++a->gen;  // the caller may write through the raw pointer: cached copies are stale
     *out = a->dptr;
     return TT_OK;
 }
@@ -845,6 +887,8 @@ tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_ar
             if (st != TT_OK) return st;
             ra[i].dptr = a->dptr;
             ra[i].bytes = a->bytes;
+            ra[i].base = args[i].v.ptr.base;
+            ra[i].gen = a->gen;
         } else if (args[i].kind < TT_ARG_I32 || args[i].kind > TT_ARG_PTR) {
             return fail(ctx, TT_ERR_INVALID, "bad tt_arg kind");
         }
@@ -885,6 +929,10 @@ tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_ar
     DeviceGuard guard(ctx->device);
     LaunchOutcome o = nk.fn(*ctx, *cfg, ra);
     if (o.status != TT_OK) return fail(ctx, o.status, o.error);
+
+    if (!o.trap.trapped)
+        for (int i = 0; i < nargs; ++i)
+            if (nk.decl.params[i].written) ++ctx->allocs[args[i].v.ptr.base].gen;
 
     // Counting and the launch log, driver.hpp:235-246 (traps count too).
     ++ctx->c.launches;
@@ -966,8 +1014,13 @@ static tt_status check_desc(const tt_trace_desc* d) {
     if (d->n < 1 || d->n > (d->full ? tt::max_full_n() : 32768))
         return fail(nullptr, TT_ERR_LAUNCH_CONFIG, "LaunchConfigError: n out of range for the native kernel");
     if (d->a_count < 0 || d->a0 < 0) return fail(nullptr, TT_ERR_INVALID, "negative angle range");
+    if (d->pair_stride > 0 && d->a_count % 2 != 0)
+        return fail(nullptr, TT_ERR_INVALID, "explicit pair_stride needs an even a_count");
+    if ((long long)d->a_count * d->n >= (1ll << 31)) return fail(nullptr, TT_ERR_INVALID, "launch too large");
     if (!d->ctab || !d->stab || !d->out || (d->full && !d->wtab))
         return fail(nullptr, TT_ERR_INVALID, "null table or output pointer");
+    if (d->full && (reinterpret_cast<std::uintptr_t>(d->wtab) & 15u))
+        return fail(nullptr, TT_ERR_INVALID, "wtab must be 16-byte aligned");
     return TT_OK;
 }
 
@@ -976,7 +1029,15 @@ static tt::TraceArgs to_args(const tt_trace_desc* d) {
     ta.img = d->img;
     ta.n = d->n;
     ta.a0 = d->a0;
-    ta.a_count = d->a_count;
+    if (d->pair_stride == 0) {
+        tt::launch_structure(d->a_count, &ta.a_count, &ta.pair_stride);
+    } else if (d->pair_stride > 0 && d->a_count % 2 == 0) {
+        ta.a_count = d->a_count / 2;
+        ta.pair_stride = d->pair_stride;
+    } else {
+        ta.a_count = d->a_count;
+        ta.pair_stride = 0;
+    }
     ta.ctab = d->ctab;
     ta.stab = d->stab;
     ta.wtab = d->wtab;

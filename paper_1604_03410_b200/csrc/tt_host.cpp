@@ -45,11 +45,10 @@ extern "C" tt_status tt_make_tables(int n, int a_total, float* ctab, float* stab
         if (stab) stab[a] = float(std::sin(theta));
     }
     if (wtab == nullptr) return TT_OK;
-    const std::size_t N = std::size_t(n);
     for (int r = 0; r < n; ++r) {
         double re3 = 0, im3 = 0, re4 = 0, im4 = 0, re5 = 0, im5 = 0;
+        const double rr = double(r);
         if (r > 0) {
-            const double rr = double(r);
             const double lg = std::log(rr);
             const double sq = std::sqrt(rr);
             re3 = rr * std::cos(5.0 * lg);
@@ -59,12 +58,15 @@ extern "C" tt_status tt_make_tables(int n, int a_total, float* ctab, float* stab
             re5 = sq * std::cos(4.0 * lg);
             im5 = sq * std::sin(4.0 * lg);
         }
-        wtab[r] = float(re3);
-        wtab[N + r] = float(im3);
-        wtab[2 * N + r] = float(re4);
-        wtab[3 * N + r] = float(im4);
-        wtab[4 * N + r] = float(re5);
-        wtab[5 * N + r] = float(im5);
+        float* e = wtab + 8 * std::size_t(r);  // [n][8] (spec §2.2)
+        e[0] = float(rr);
+        e[1] = float(rr * rr);
+        e[2] = float(re3);
+        e[3] = float(im3);
+        e[4] = float(re4);
+        e[5] = float(im4);
+        e[6] = float(re5);
+        e[7] = float(im5);
     }
     return TT_OK;
 }

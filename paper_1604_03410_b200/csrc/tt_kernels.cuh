@@ -26,12 +26,13 @@ struct TraceArgs {
     cudaTextureObject_t tex = 0;  // same image as a 2-D texture (Sampler::Texture)
     int n = 0;                    // image side == line length == lines per angle
     int a0 = 0;                   // first angle (index into ctab/stab)
-    int a_count = 0;              // angles in this launch
+    int a_count = 0;              // launch units (angles a0 .. a0+a_count-1)
+    int pair_stride = 0;          // >0: unit i also owns angle a0+i+pair_stride (rows a_count+i)
     const float* ctab = nullptr;  // [A_total] cos(theta_a), f64 -> f32 on host
     const float* stab = nullptr;  // [A_total] sin(theta_a)
-    const float* wtab = nullptr;  // [6][n] planar complex weight tables (spec §2.2)
-    float* out = nullptr;         // full: [a_count][6][n]; T0-only: [a_count][n]
-    int32_t* med = nullptr;       // full: [a_count][2][n] (m, m'), may be null
+    const float* wtab = nullptr;  // [n][8]: r, r^2, w3re, w3im, w4re, w4im, w5re, w5im (spec §2.2), 16-B aligned
+    float* out = nullptr;         // full: [rows][6][n]; T0-only: [rows][n]; rows = a_count*(1+paired)
+    int32_t* med = nullptr;       // full: [rows][2][n] (m, m'), may be null
     bool full = true;             // T0..T5 (else T0 / Radon only)
     Sampler sampler = Sampler::Global;
 };
@@ -39,6 +40,18 @@ struct TraceArgs {
 // Warps per line of the fused kernel for side n — part of the reduction
 // schedule that oracle/tt_oracle.c TTO_REPLAY mirrors.
 int schedule_warps(int n);
+
+// Launch units for a drop-in launch of a_count angles: pairs (i, i+a_count/2)
+// when a_count is even (the kernel pairs mirrored angles).
+inline void launch_structure(int a_count, int* units, int* pair_stride) {
+    if (a_count >= 2 && a_count % 2 == 0) {
+        *units = a_count / 2;
+        *pair_stride = a_count / 2;
+    } else {
+        *units = a_count;
+        *pair_stride = 0;
+    }
+}
 
 // Largest n the fused T0-T5 kernel supports (line buffer must fit in smem).
 int max_full_n();

@@ -26,10 +26,10 @@ RADON = KernelAst("radon", ["img", "n", "ctab", "stab", "out", "a0"])
 
 
 def make_tables(n: int, a_total: int):
-    """ctab, stab [a_total] and wtab [6n]."""
+    """ctab, stab [a_total] and wtab [n][8]."""
     c = np.empty(a_total, np.float32)
     s = np.empty(a_total, np.float32)
-    w = np.empty(6 * n, np.float32)
+    w = np.empty(8 * n, np.float32)
     _check(lib.tt_make_tables(n, a_total, c.ctypes.data, s.ctypes.data, w.ctypes.data))
     return c, s, w
 
@@ -145,10 +145,10 @@ class TraceTransform:
 
 def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, stab_ptr: int, wtab_ptr: int,
                  out_ptr: int, med_ptr: int = 0, full: bool = True, sampler: int = 0, stream: int = 0,
-                 tex=None) -> None:
-    """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex)."""
+                 tex=None, pair_stride: int = 0) -> None:
+    """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex); pair_stride as in tt_b200.h."""
     d = _lib.TraceDesc(img_ptr, n, a0, a_count, int(full), ctab_ptr, stab_ptr, wtab_ptr or None, out_ptr,
-                       med_ptr or None, sampler, 0)
+                       med_ptr or None, sampler, pair_stride)
     if tex is not None:
         _check(lib.tt_trace_device_tex(C.byref(d), tex, C.c_void_p(stream)))
     else:

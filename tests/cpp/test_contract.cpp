@@ -87,7 +87,7 @@ int main() {
     {  // the path: trace_t05 through cuda_launch, bit-exact vs the replay oracle
         DeviceContext ctx = create_context();
         const int n = 192, A = 45;
-        std::vector<float> img(size_t(n) * n), ctab(A), stab(A), wtab(6 * size_t(n));
+        std::vector<float> img(size_t(n) * n), ctab(A), stab(A), wtab(8 * size_t(n));
         tt_synth_image(1, 7, n, img.data());
         tt_make_tables(n, A, ctab.data(), stab.data(), wtab.data());
         std::vector<float> out(size_t(A) * 6 * n);

@@ -152,7 +152,7 @@ def test_trace_transform_one_call_flow_counts(ctx):
     img = tt.synth_image(tt.DISK, n)
     out, med, rep = tr(img)
     assert rep.ok() and not rep.cache_hit
-    assert rep.bytes_h2d == n * n * 4 + 2 * A * 4 + 6 * n * 4
+    assert rep.bytes_h2d == n * n * 4 + 2 * A * 4 + 8 * n * 4
     assert rep.bytes_d2h == A * 6 * n * 4 + A * 2 * n * 4
     out2, med2, rep2 = tr(img)
     assert rep2.cache_hit and np.array_equal(out, out2) and np.array_equal(med, med2)

@@ -252,7 +252,7 @@ def test_trace_launch_contract(ctx):
                                           (True, "f32"), (True, "f32"), (True, "i32"), (False, "i32")], "t")
     fn = ctx.get_function(ctx.module_load(mod), "trace_t05")
     c, s, w = tt.make_tables(n, A)
-    bufs = [ctx.mem_alloc(x) for x in (n * n * 4, A * 4, A * 4, 6 * n * 4, A * 6 * n * 4, A * 2 * n * 4)]
+    bufs = [ctx.mem_alloc(x) for x in (n * n * 4, A * 4, A * 4, 8 * n * 4, A * 6 * n * 4, A * 2 * n * 4)]
     for b, h in zip(bufs[1:4], (c, s, w)):
         ctx.memcpy_htod(b, h)
     img, ct, st, wt, out, med = bufs

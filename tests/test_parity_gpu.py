@@ -74,15 +74,69 @@ def test_radon_equals_t0_of_full_kernel(ctx):
     assert _bitwise_equal(full[:, 0, :], t0[:, 0, :])
 
 
-def test_angle_shard_equals_slice_of_whole(ctx):
-    """Orientation sharding (a0, a_count) reproduces the unsharded slice exactly."""
+def test_dropin_angle_subrange_bit_exact(ctx):
+    """A drop-in launch of an angle sub-range (a0, a_count) replays exactly."""
     n, A = 200, 24
     img = tt.synth_image(tt.DISK, n)
-    _, whole, wmed = _run(ctx, img, n, A)
     for a0, cnt in [(0, 6), (6, 6), (12, 11), (23, 1)]:
-        _, part, pmed = _run(ctx, img, n, A, a0=a0, a_count=cnt)
-        assert _bitwise_equal(part, whole[a0:a0 + cnt])
-        assert np.array_equal(pmed, wmed[a0:a0 + cnt])
+        tr, part, pmed = _run(ctx, img, n, A, a0=a0, a_count=cnt)
+        rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, a0=a0, a_count=cnt, mode=O.REPLAY)
+        assert _bitwise_equal(part, rout) and np.array_equal(pmed, rmed)
+
+
+def _raw(ctx, img, n, c, s, w, a0, a_count, pair_stride, full=True, sampler=0):
+    """tt_trace_device on context-owned buffers (the multi-GPU driver's entry)."""
+    F = 6 if full else 1
+    bufs = {k: ctx.mem_alloc(x.nbytes) for k, x in (("img", img), ("c", c), ("s", s), ("w", w))}
+    for k, x in (("img", img), ("c", c), ("s", s), ("w", w)):
+        ctx.memcpy_htod(bufs[k], np.ascontiguousarray(x))
+    out_d = ctx.mem_alloc(a_count * F * n * 4)
+    med_d = ctx.mem_alloc(a_count * 2 * n * 4)
+    ptr = {k: ctx.device_pointer(v) for k, v in bufs.items()}
+    tt.trace_device(ptr["img"], n, a0, a_count, ptr["c"], ptr["s"], ptr["w"], ctx.device_pointer(out_d),
+                    ctx.device_pointer(med_d), full=full, sampler=sampler, stream=ctx.stream,
+                    pair_stride=pair_stride)
+    ctx.synchronize()
+    out = np.empty((a_count, F, n), np.float32)
+    med = np.empty((a_count, 2, n), np.int32)
+    ctx.memcpy_dtoh(out, out_d)
+    ctx.memcpy_dtoh(med, med_d)
+    for b in list(bufs.values()) + [out_d, med_d]:
+        ctx.mem_free(b)
+    return out, med
+
+
+@pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
+def test_orientation_shards_with_mirror_halves_are_exact_slices(ctx, sampler):
+    """Multi-GPU sharding (row e): rank r of G takes angles [r*A/2G, (r+1)*A/2G)
+    plus their mirrors (pair_stride = A/2); the shards are bit-identical to the
+    corresponding rows of the single-launch transform."""
+    n, A, G = 160, 48, 4
+    img = tt.synth_image(tt.PHANTOM, n)
+    c, s, w = tt.make_tables(n, A)
+    whole, wmed = _raw(ctx, img, n, c, s, w, 0, A, 0, sampler=sampler)
+    rout, rmed, _, _ = O.transform(img, n, c, s, w, mode=O.REPLAY)
+    assert _bitwise_equal(whole, rout) and np.array_equal(wmed, rmed)
+    h = A // 2
+    for r in range(G):
+        a0, cnt = r * h // G, (r + 1) * h // G - r * h // G
+        part, pmed = _raw(ctx, img, n, c, s, w, a0, 2 * cnt, h, sampler=sampler)
+        assert _bitwise_equal(part[:cnt], whole[a0:a0 + cnt])
+        assert _bitwise_equal(part[cnt:], whole[h + a0:h + a0 + cnt])
+        assert np.array_equal(pmed[:cnt], wmed[a0:a0 + cnt]) and np.array_equal(pmed[cnt:], wmed[h + a0:h + a0 + cnt])
+        ro, rm = O.replay_launch(img, n, c, s, w, a0=a0, units=cnt, pair_stride=h)
+        assert _bitwise_equal(part, ro) and np.array_equal(pmed, rm)
+
+
+def test_unpaired_raw_launch_matches_unpaired_replay(ctx):
+    n, A = 96, 10
+    img = tt.synth_image(tt.SPARSE, n)
+    c, s, w = tt.make_tables(n, A)
+    out, med = _raw(ctx, img, n, c, s, w, 0, A, -1)
+    ro, rm = O.replay_launch(img, n, c, s, w, a0=0, units=A, pair_stride=0)
+    assert _bitwise_equal(out, ro) and np.array_equal(med, rm)
+    fails, st = O.check(img, n, c, s, w, out, med)
+    assert fails == 0, st
 
 
 def test_zero_image_gives_zero_functionals_and_zero_medians(ctx):
@@ -158,3 +212,49 @@ def test_size_independent_properties_at_8192(ctx):
     assert mask.sum() > n // 2
     assert np.max(np.abs(t0[mask] - t0r[mask]) / t0[mask]) < 1e-3
     assert np.all(out[:, 1:] >= 0)
+
+
+def test_texture_cache_follows_image_rewrites(ctx):
+    """The texture sampler caches a block-linear copy per image allocation; every
+    write to the allocation (H2D copy, a kernel storing into it) must refresh it."""
+    n, A = 128, 8
+    ctx.set_sampler(1)
+    tr = tt.TraceTransform(ctx, n, A)
+    out = np.empty(tr.out_shape(), np.float32)
+    med = np.empty((A, 2, n), np.int32)
+    imgs = [tt.synth_image(k, n) for k in (tt.DISK, tt.PHANTOM, tt.SPARSE)]
+    for img in imgs + imgs[:1]:
+        tr.run_resident(img, out, med)
+        ref, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+        assert _bitwise_equal(out, ref) and np.array_equal(med, rmed)
+    # a native kernel writing into the image buffer (scale by 2) also invalidates the copy
+    img = imgs[1]
+    tr.run_resident(img, out, med)
+    mod = ctx.module_load(tt.render_module(tt.KernelAst("scale", ["a", "k"]), [(True, "f32"), (False, "f32")], "s"))
+    fn = ctx.get_function(mod, "scale")
+    r = tr._resident()
+    flat = tt.GridConfig((1, 1, 1), (1, 1, 1))
+    ctx.memcpy_htod(r["img"], (img * np.float32(2.0)).astype(np.float32))
+    tr.launch_resident()
+    ctx.memcpy_dtoh(out, r["out"])
+    ref, _, _, _ = O.transform((img * np.float32(2.0)).astype(np.float32), n, tr.ctab, tr.stab, tr.wtab,
+                               mode=O.REPLAY)
+    assert _bitwise_equal(out, ref)
+    assert ctx.launch(fn, flat, [r["img"], np.float32(0.5)]).ok()  # kernel write -> generation bump
+    tr.launch_resident()
+    ctx.memcpy_dtoh(out, r["out"])
+    img2 = (img * np.float32(2.0)).astype(np.float32)
+    img2.reshape(-1)[0] = img2.reshape(-1)[0] * np.float32(0.5)
+    ref, _, _, _ = O.transform(img2, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+    assert _bitwise_equal(out, ref)
+    ctx.set_sampler(0)
+
+
+def test_tiny_and_denormal_values_exact(ctx):
+    """sqrt of zero / denormal / tiny samples (the kernel's exact fast sqrt path)."""
+    n, A = 64, 6
+    img = (tt.synth_image(tt.DISK, n) * np.float32(1e-38)).astype(np.float32)
+    for sampler in (0, 1):
+        tr, out, med = _run(ctx, img, n, A, sampler=sampler)
+        rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+        assert _bitwise_equal(out, rout) and np.array_equal(med, rmed)
