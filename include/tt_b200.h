@@ -165,7 +165,7 @@ tt_status tt_ctx_synchronize(tt_ctx* ctx);
 tt_status tt_ctx_stream(tt_ctx* ctx, void** stream_out); /* cudaStream_t for interop */
 tt_status tt_ctx_device(const tt_ctx* ctx, int* device_out);
 /* Extension: image sampler of this context's trace launches:
- * 0 = global/L1 loads (default), 1 = texture gather (TLD4). */
+ * 0 = global/L1 loads, 1 = texture gather (TLD4, default). */
 tt_status tt_ctx_set_sampler(tt_ctx* ctx, int sampler);
 
 /* ---- modules and functions (driver.hpp:138-177) ------------------------------ */
@@ -240,6 +240,11 @@ typedef struct tt_trace_desc {
     int32_t pair_stride;
 } tt_trace_desc;
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
+
+/* P-functionals (circus features) of `rows` sinogram rows of
+ * length n on device: circ[row][3] = (total variation, value at the weighted
+ * median, max).  For a trace output [a][6][n], rows = 6a. */
+tt_status tt_circus_device(const float* d_sino, int n, int rows, float* d_circ, void* stream);
 
 /* Prepared texture for repeated tt_trace_device calls on one image
  * (sampler 1 without the per-call copy). */

@@ -55,6 +55,9 @@ def lib():
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, ip, dp, dp, ctypes.c_int]
         L.tto_replay_launch.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
                                         ctypes.c_int, ctypes.c_int, fp, ip, ctypes.c_int]
+        L.tto_circus.argtypes = [fp, ctypes.c_int, ctypes.c_int, fp, dp, ip, ctypes.c_int]
+        L.tto_is_eps_median.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_double]
+        L.tto_is_eps_median.restype = ctypes.c_int
         L.tto_line_f64.argtypes = [fp, ctypes.c_int, fp, ctypes.c_int, ctypes.c_int, dp, dp, ip]
         L.tto_check.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
                                 ctypes.c_int, fp, ip, ctypes.c_double, ctypes.c_int, ctypes.c_double, dp, ctypes.c_int]
@@ -121,6 +124,23 @@ def replay_launch(img, n, ctab, stab, wtab, *, a0, units, pair_stride, full=True
     lib().tto_replay_launch(_f(np.ascontiguousarray(img, np.float32)), n, a0, units, pair_stride, _f(ctab),
                             _f(stab), _f(wtab), int(full), W, _f(out), _p(med, ctypes.c_int32), nthreads)
     return out, (med if full else None)
+
+
+def circus(sino, nthreads=0):
+    """P-functionals of sinogram rows: returns (replay f32 [..., 3], f64 truth [..., 3], median idx)."""
+    sino = np.ascontiguousarray(sino, np.float32)
+    n = sino.shape[-1]
+    rows = sino.size // n
+    c = np.empty(sino.shape[:-1] + (3,), np.float32)
+    c64 = np.empty(sino.shape[:-1] + (3,), np.float64)
+    med = np.empty(sino.shape[:-1], np.int32)
+    lib().tto_circus(_f(sino), n, rows, _f(c), _p(c64, ctypes.c_double), _p(med, ctypes.c_int32), nthreads)
+    return c, c64, med
+
+
+def is_eps_median(v, m, eps):
+    v = np.ascontiguousarray(v, np.float32)
+    return bool(lib().tto_is_eps_median(_f(v), v.size, int(m), float(eps)))
 
 
 def check(img, n, ctab, stab, wtab, gpu_out, gpu_med=None, *, a0=0, full=True, rtol=1e-4, W=0, chain=0.0,

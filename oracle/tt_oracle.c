@@ -142,12 +142,11 @@ void tto_line_samples(const float* img, int n, float c, float s, int p, float* v
 }
 
 /* Mirrors tt::schedule_warps (paper_1604_03410_b200/csrc/tt_kernels.cu):
- * the largest power of two <= n/512, clamped to [1, 16]. */
+ * the smallest power of two W with ceil(n / 32W) <= 32, clamped to [1, 16]. */
 int tto_schedule_warps(int n) {
-    int w = n / 512, p = 1;
-    if (w < 1) return 1;
-    while (p * 2 <= w && p < 16) p *= 2;
-    return p;
+    int w = 1;
+    while (w * 1024 < n && w < 16) w *= 2;
+    return w;
 }
 
 /* ----------------------------------------------------- f64 truth (§2.5) */
@@ -302,6 +301,25 @@ static int replay_rescan(const float* u, int n, int start, int K, float exc, flo
     return len > 0 ? start + len - 1 : n - 1;
 }
 
+/* Chunk sum rule of the kernel: balanced pairwise tree
+ * (left + right) over a full power-of-two chunk, else sequential. */
+static float tree_sum(const float* u, int K) {
+    if (K == 1) return u[0];
+    const float l = tree_sum(u, K / 2);
+    const float r = tree_sum(u + K / 2, K / 2);
+    return l + r;
+}
+
+static float chunk_sum(const float* u, int n, int start, int K) {
+    int len = n - start;
+    if (len > K) len = K;
+    if (len <= 0) return 0.0f;
+    if (len == K && (K & (K - 1)) == 0) return tree_sum(u + start, K);
+    float acc = 0.0f;
+    for (int t = start; t < start + len; ++t) acc = acc + u[t];
+    return acc;
+}
+
 /* Weighted median of u under the kernel's schedule. */
 static int replay_median(const float* u, int n, float S, int W) {
     const int nslot = 32 * W;
@@ -310,11 +328,8 @@ static int replay_median(const float* u, int n, float S, int W) {
     for (int w = 0; w < W; ++w) {
         float c[32], inc[32];
         for (int l = 0; l < 32; ++l) {
-            int k = 32 * w + l;
-            float acc = 0.0f;
-            for (int t = k * K; t < n && t < (k + 1) * K; ++t) acc = acc + u[t];
-            c[l] = acc;
-            inc[l] = acc;
+            c[l] = chunk_sum(u, n, (32 * w + l) * K, K);
+            inc[l] = c[l];
         }
         warp_scan(inc);
         for (int l = 0; l < 32; ++l) {
@@ -514,9 +529,57 @@ void tto_transform(const float* img, int n, int a0, int a_count, int a_total, co
     }
 }
 
+/* ----------------------------------------------- P-functionals (§2.7) */
+
+void tto_circus(const float* sino, int n, int rows, float* circ, double* circ64, int32_t* med, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel
+    {
+        float* d = (float*)malloc(sizeof(float) * (size_t)(n > 1 ? n : 1));
+#pragma omp for schedule(dynamic, 16)
+        for (int row = 0; row < rows; ++row) {
+            const float* s = sino + (size_t)row * n;
+            for (int p = 0; p + 1 < n; ++p) d[p] = fabsf(s[p + 1] - s[p]);
+            const float S = replay_strided_sum(s, n, 1);
+            const float P1 = replay_strided_sum(d, n - 1 > 0 ? n - 1 : 0, 1);
+            const int m = replay_median(s, n, S, 1);
+            float mx = 0.0f;
+            for (int p = 0; p < n; ++p) mx = fmaxf(mx, s[p]);
+            if (circ) {
+                circ[(size_t)row * 3 + 0] = P1;
+                circ[(size_t)row * 3 + 1] = n > 0 ? s[m] : 0.0f;
+                circ[(size_t)row * 3 + 2] = mx;
+            }
+            if (med) med[row] = m;
+            if (circ64) {
+                double tv = 0.0, tot = 0.0, P = 0.0;
+                for (int p = 0; p + 1 < n; ++p) tv += fabs((double)s[p + 1] - (double)s[p]);
+                for (int p = 0; p < n; ++p) tot += (double)s[p];
+                int m64 = 0;
+                if (tot > 0.0)
+                    for (int p = 0; p < n; ++p) {
+                        P += (double)s[p];
+                        if (2.0 * P >= tot) { m64 = p; break; }
+                    }
+                circ64[(size_t)row * 3 + 0] = tv;
+                circ64[(size_t)row * 3 + 1] = n > 0 ? (double)s[m64] : 0.0;
+                circ64[(size_t)row * 3 + 2] = (double)mx;
+            }
+        }
+        free(d);
+    }
+}
+
 /* --------------------------------------------------------------- checker */
+static int is_eps_median(const float* v, int n, int m, double eps);
 
 /* Is m an eps-median of v (f64 prefix)?  spec §2.5 */
+int tto_is_eps_median(const float* v, int n, int m, double eps) { return is_eps_median(v, n, m, eps); }
+
 static int is_eps_median(const float* v, int n, int m, double eps) {
     if (m < 0 || m >= n) return 0;
     double S = 0.0;

@@ -85,6 +85,15 @@ void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stri
  * angles: pairs (i, i + a_count/2) when a_count is even. */
 void tto_launch_structure(int a_count, int* units, int* pair_stride);
 
+/* P-functionals of sinogram rows (spec §2.7): circ[row][3] = P1 (total
+ * variation), P2 (value at the weighted median), P3 (max) under the kernel's
+ * one-warp schedule (bit-exact replay); circ64 the f64 truth (P2 at the f64
+ * median); med[row] the replayed median index.  Any output may be NULL. */
+void tto_circus(const float* sino, int n, int rows, float* circ, double* circ64, int32_t* med, int nthreads);
+
+/* 1 if m is an eps-median of v (f64 prefix), the tie rule of spec §2.5. */
+int tto_is_eps_median(const float* v, int n, int m, double eps);
+
 /* Per-line truth evaluated at forced medians (tie re-evaluation, §2.5).
  * m_force / mp_force < 0 -> use the f64 medians. */
 void tto_line_f64(const float* v, int n, const float* wtab, int m_force, int mp_force,

@@ -93,6 +93,7 @@ _sigs = {
     "tt_count_inbounds_taps": (C.c_uint64, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_ffma_probe": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "tt_trace_device": (_S, [C.POINTER(TraceDesc), C.c_void_p]),
+    "tt_circus_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_image_tex_create": (_S, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     "tt_image_tex_destroy": (_S, [C.c_void_p]),
     "tt_trace_device_tex": (_S, [C.POINTER(TraceDesc), C.c_void_p, C.c_void_p]),

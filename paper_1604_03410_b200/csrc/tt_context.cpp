@@ -146,7 +146,7 @@ struct tt_ctx {
     tt_caps caps{1024, 48 * 1024};
     bool destroyed = false;
     cudaStream_t stream = nullptr;
-    int sampler = 0;  // tt::Sampler for trace launches (TT_SAMPLER env: "tex" -> 1)
+    int sampler = 1;  // tt::Sampler for trace launches (default texture; TT_SAMPLER=ldg -> 0)
 
     std::map<std::uint64_t, Module> modules;
     std::map<std::uint64_t, FunctionEntry> functions;
@@ -536,6 +536,21 @@ LaunchOutcome run_radon(tt_ctx& ctx, const tt_grid& g, const std::vector<Resolve
     return run_trace_common(ctx, g, a[0], a[1].value.v.i32, a[2], a[3], nullptr, a[4], nullptr, a[5].value.v.i32, false);
 }
 
+// circus(sino, n, rows, circ): P-functionals of `rows` sinogram rows of length
+// n -> circ[rows][3]; the consumer stage of trace_t05.
+LaunchOutcome run_circus(tt_ctx& ctx, const tt_grid&, const std::vector<ResolvedArg>& a) {
+    LaunchOutcome o;
+    const int n = a[1].value.v.i32, rows = a[2].value.v.i32;
+    if (n <= 0 || rows <= 0) return o;
+    if (elems(a[0], 4) < std::uint64_t(n) * std::uint64_t(rows) || elems(a[3], 4) < 3ull * std::uint64_t(rows)) {
+        o.trap = first_thread_trap(TT_TRAP_GLOBAL_OUT_OF_BOUNDS);
+        return o;
+    }
+    o = cuda_outcome(tt::launch_circus((const float*)a[0].dptr, n, rows, (float*)a[3].dptr, ctx.stream), "circus");
+    o.gpu_launches = 1;
+    return o;
+}
+
 Param P(bool ptr, Scalar t, const char* name, bool written = false) {
     Param p;
     p.ptr = ptr;
@@ -564,6 +579,8 @@ const std::vector<NativeKernel>& registry() {
             {P(true, f, "img"), P(false, i, "n"), P(true, f, "ctab"), P(true, f, "stab"), P(true, f, "out", true),
              P(false, i, "a0")},
             run_radon);
+        add("circus", {P(true, f, "sino"), P(false, i, "n"), P(false, i, "rows"), P(true, f, "circ", true)},
+            run_circus);
         add("vadd", {P(true, f, "a"), P(true, f, "b"), P(true, f, "c", true)}, run_vadd<tt::ElemKind::F32, 4>);
         add("vadd", {P(true, d, "a"), P(true, d, "b"), P(true, d, "c", true)}, run_vadd<tt::ElemKind::F64, 8>);
         add("vadd", {P(true, i, "a"), P(true, i, "b"), P(true, i, "c", true)}, run_vadd<tt::ElemKind::I32, 4>);
@@ -647,8 +664,10 @@ tt_status tt_ctx_create(int device, const tt_caps* caps, tt_ctx** out) {
         std::uint64_t thresh = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
     }
+    // Texture gather is the default sampler (measured faster, profiles/); TT_SAMPLER=ldg selects L1 loads.
+    ctx->sampler = 1;
     const char* smp = std::getenv("TT_SAMPLER");
-    if (smp && (std::strcmp(smp, "tex") == 0 || std::strcmp(smp, "1") == 0)) ctx->sampler = 1;
+    if (smp && (std::strcmp(smp, "ldg") == 0 || std::strcmp(smp, "0") == 0)) ctx->sampler = 0;
     ctx->id = ++g_next_ctx_id;
     *out = ctx.release();
     return TT_OK;
@@ -1077,6 +1096,12 @@ struct tt_image_tex {
 };
 
 extern "C" {
+
+tt_status tt_circus_device(const float* d_sino, int n, int rows, float* d_circ, void* stream) {
+    if (!d_sino || !d_circ || n < 1 || rows < 0) return fail(nullptr, TT_ERR_INVALID, "bad circus arguments");
+    cudaError_t e = tt::launch_circus(d_sino, n, rows, d_circ, (cudaStream_t)stream);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "circus");
+}
 
 tt_status tt_image_tex_create(const float* d_img, int n, void* stream, tt_image_tex** out) {
     if (!d_img || !out || n < 1) return fail(nullptr, TT_ERR_INVALID, "bad argument");

@@ -84,6 +84,11 @@ cudaError_t make_image_texture(const float* img, int n, cudaStream_t s, cudaArra
 // FP32 roofline probe: blocks x 256 threads x iters x 128 FFMA (2 flop each).
 cudaError_t launch_ffma_probe(float* out, int blocks, int iters, cudaStream_t s);
 
+// P-functionals (circus features) of `rows` sinogram rows of length n:
+// circ[row][3] = (P1 total variation, P2 weighted-median value, P3 max),
+// DESIGN.md §2.7.  One warp per row.
+cudaError_t launch_circus(const float* sino, int n, int rows, float* circ, cudaStream_t s);
+
 // Writes a buffer larger than L2 (timing hygiene between bench iterations).
 cudaError_t launch_l2_flush(void* buf, uint64_t bytes, cudaStream_t s);
 

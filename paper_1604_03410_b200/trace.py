@@ -22,6 +22,7 @@ SEEDS = {DISK: 20160412, PHANTOM: 7, SPARSE: 11}
 NF = 6
 
 TRACE_T05 = KernelAst("trace_t05", ["img", "n", "ctab", "stab", "wtab", "out", "med", "a0"])
+CIRCUS = KernelAst("circus", ["sino", "n", "rows", "circ"])
 RADON = KernelAst("radon", ["img", "n", "ctab", "stab", "out", "a0"])
 
 
@@ -62,8 +63,9 @@ class TraceTransform:
     image in and the sinograms out (the e2e benchmark path)."""
 
     def __init__(self, ctx: DeviceContext, n: int, angles: int, full: bool = True, a0: int = 0,
-                 a_count: int | None = None):
+                 a_count: int | None = None, features: bool = False):
         self.ctx, self.n, self.angles, self.full = ctx, n, angles, full
+        self.features = features and full  # P-functional (circus) stage after the trace kernel
         self.a0 = a0
         self.a_count = angles - a0 if a_count is None else a_count
         self.ctab, self.stab, self.wtab = make_tables(n, angles)
@@ -98,7 +100,8 @@ class TraceTransform:
             r = {"img": ctx.mem_alloc(self.n * self.n * 4), "ctab": ctx.mem_alloc(self.ctab.nbytes),
                  "stab": ctx.mem_alloc(self.stab.nbytes), "wtab": ctx.mem_alloc(self.wtab.nbytes),
                  "out": ctx.mem_alloc(int(np.prod(self.out_shape())) * 4),
-                 "med": ctx.mem_alloc(self.a_count * 2 * self.n * 4)}
+                 "med": ctx.mem_alloc(self.a_count * 2 * self.n * 4),
+                 "circ": ctx.mem_alloc(self.a_count * NF * 3 * 4)}
             ctx.memcpy_htod(r["ctab"], self.ctab)
             ctx.memcpy_htod(r["stab"], self.stab)
             ctx.memcpy_htod(r["wtab"], self.wtab)
@@ -109,6 +112,9 @@ class TraceTransform:
             from .api import render_module
             mh = ctx.module_load(render_module(kern, types, kern.name + "$resident"))
             r["fn"] = ctx.get_function(mh, kern.name)
+            mc = ctx.module_load(render_module(CIRCUS, [(True, "f32"), (False, "i32"), (False, "i32"), (True, "f32")],
+                                               "circus$resident"))
+            r["circus"] = ctx.get_function(mc, "circus")
             self._res = r
         return self._res
 
@@ -123,22 +129,30 @@ class TraceTransform:
         res = self.ctx.launch(r["fn"], self.cfg, args)
         if not res.ok():
             raise RuntimeError(f"trace launch trapped: {res.trap}")
+        if self.features:
+            rows = self.a_count * NF
+            res = self.ctx.launch(r["circus"], GridConfig(((rows + 7) // 8, 1, 1), (256, 1, 1)),
+                                  [r["out"], np.int32(self.n), np.int32(rows), r["circ"]])
+            if not res.ok():
+                raise RuntimeError(f"circus launch trapped: {res.trap}")
 
-    def run_resident(self, img_host, out_host, med_host=None):
-        """H2D image -> fused kernel -> D2H sinograms (+ medians)."""
+    def run_resident(self, img_host, out_host, med_host=None, circ_host=None):
+        """H2D image -> fused kernel (-> circus) -> D2H sinograms (+ medians, + features)."""
         r = self._resident()
         self.ctx.memcpy_htod(r["img"], img_host, self.n * self.n * 4)
         self.launch_resident()
         self.ctx.memcpy_dtoh(out_host, r["out"], int(np.prod(self.out_shape())) * 4)
         if med_host is not None and self.full:
             self.ctx.memcpy_dtoh(med_host, r["med"], self.a_count * 2 * self.n * 4)
+        if circ_host is not None and self.features:
+            self.ctx.memcpy_dtoh(circ_host, r["circ"], self.a_count * NF * 3 * 4)
 
     def resident_ptr(self, name: str) -> int:
         return self.ctx.device_pointer(self._resident()[name])
 
     def free_resident(self):
         if self._res is not None:
-            for k in ("img", "ctab", "stab", "wtab", "out", "med"):
+            for k in ("img", "ctab", "stab", "wtab", "out", "med", "circ"):
                 self.ctx.mem_free(self._res[k])
             self._res = None
 
@@ -153,6 +167,24 @@ def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, sta
         _check(lib.tt_trace_device_tex(C.byref(d), tex, C.c_void_p(stream)))
     else:
         _check(lib.tt_trace_device(C.byref(d), C.c_void_p(stream)))
+
+
+def circus_device(sino_ptr: int, n: int, rows: int, circ_ptr: int, stream: int = 0) -> None:
+    """P-functionals of `rows` device sinogram rows (tt_circus_device)."""
+    _check(lib.tt_circus_device(C.c_void_p(sino_ptr), n, rows, C.c_void_p(circ_ptr), C.c_void_p(stream)))
+
+
+def circus(ctx: DeviceContext, sino: np.ndarray):
+    """P-functionals of host sinogram rows through cuda_launch (circus kernel)."""
+    sino = np.ascontiguousarray(sino, np.float32)
+    n = sino.shape[-1]
+    rows = sino.size // n
+    circ = np.empty(sino.shape[:-1] + (3,), np.float32)
+    rep = cuda_launch(ctx, CIRCUS, GridConfig(((rows + 7) // 8, 1, 1), (256, 1, 1)),
+                      [cu_in(sino), np.int32(n), np.int32(rows), cu_out(circ)])
+    if not rep.ok():
+        raise RuntimeError(f"circus launch trapped: {rep.trap}")
+    return circ
 
 
 def image_texture(img_ptr: int, n: int, stream: int = 0):

@@ -1,0 +1,65 @@
+"""P-functionals / circus stage: bit-exact vs the oracle's
+replay of the one-warp schedule; P1/P3 within tolerance of the f64 truth and
+P2 taken at an eps-median of the f64 prefix."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1604_03410_b200 as tt
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx(gpu):
+    c = tt.create_context(gpu)
+    yield c
+    c.destroy()
+
+
+def _check_against_truth(sino, circ):
+    rc, r64, _ = O.circus(sino)
+    assert np.array_equal(circ.view(np.uint32), rc.view(np.uint32)), "differs bitwise from the replay"
+    n = sino.shape[-1]
+    chain = (n + 31) // 32 + 10
+    eps = 2 * chain * 2.0 ** -24
+    p1_err = np.abs(circ[..., 0] - r64[..., 0]) / (1e-4 * np.abs(r64[..., 0]) + 1e-30 + eps * r64[..., 0])
+    assert np.all(p1_err <= 1.0)
+    assert np.array_equal(circ[..., 2], r64[..., 2].astype(np.float32))
+    rows = sino.reshape(-1, n)
+    flat = circ.reshape(-1, 3)
+    for i in range(rows.shape[0]):  # P2 is the value at an eps-median index
+        idx = np.nonzero(rows[i] == flat[i, 1])[0]
+        assert any(O.is_eps_median(rows[i], int(m), eps) for m in idx) or (flat[i, 1] == 0 and not rows[i].any())
+
+
+@pytest.mark.parametrize("n,A,kind", [(64, 10, tt.DISK), (256, 360, tt.PHANTOM), (1000, 8, tt.SPARSE),
+                                      (1024, 24, tt.DISK)])
+def test_circus_of_trace_output(ctx, n, A, kind):
+    img = tt.synth_image(kind, n)
+    tr = tt.TraceTransform(ctx, n, A)
+    sino, _, _ = tr(img)
+    circ = tt.circus(ctx, sino)
+    assert circ.shape == (A, 6, 3)
+    _check_against_truth(sino, circ)
+
+
+def test_circus_edge_rows(ctx):
+    rng = np.random.default_rng(3)
+    sino = np.stack([np.zeros(77), np.ones(77), rng.random(77) ** 8, np.eye(1, 77, 76)[0], np.eye(1, 77, 0)[0]])
+    circ = tt.circus(ctx, sino.astype(np.float32))
+    _check_against_truth(sino.astype(np.float32), circ)
+
+
+def test_resident_flow_with_features(ctx):
+    n, A = 512, 40
+    img = tt.synth_image(tt.PHANTOM, n)
+    tr = tt.TraceTransform(ctx, n, A, features=True)
+    out = np.empty(tr.out_shape(), np.float32)
+    med = np.empty((A, 2, n), np.int32)
+    circ = np.empty((A, 6, 3), np.float32)
+    tr.run_resident(img, out, med, circ)
+    ref, _, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+    rc, _, _ = O.circus(out)
+    assert np.array_equal(circ.view(np.uint32), rc.view(np.uint32))
