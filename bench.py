@@ -35,9 +35,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    "c1": dict(n=256, angles=360, full=True, desc="256^2 fp32, 360 angles x 256 lines, T0-T5"),
-    "c2": dict(n=1024, angles=720, full=True, desc="1024^2 fp32, 720 angles x 1024 lines, T0-T5"),
-    "c3": dict(n=4096, angles=1440, full=True, desc="4096^2 fp32, 1440 angles x 4096 lines, T0-T5"),
+    "c1": dict(n=256, angles=360, full=True, features=False, desc="256^2 fp32, 360 angles x 256 lines, T0-T5"),
+    "c2": dict(n=1024, angles=720, full=True, features=True,
+               desc="1024^2 fp32, 720 angles x 1024 lines, T0-T5 + P-functionals (circus)"),
+    "c3": dict(n=4096, angles=1440, full=True, features=False, desc="4096^2 fp32, 1440 angles x 4096 lines, T0-T5"),
 }
 FLOPS_PER_TAP = {True: 34, False: 16}  # FMA = 2, in-bounds taps only
 METRIC = "trace-transform sinogram samples/s"
@@ -192,19 +193,27 @@ def run_ours(args, ws, rank, local):
         ctab, stab, wtab = (torch.from_numpy(x).cuda() for x in (ctab_h, stab_h, wtab_h))
         out = torch.empty((a_cnt, F, n), device="cuda")
         med = torch.empty((a_cnt, 2, n), dtype=torch.int32, device="cuda")
+        circ = torch.empty((a_cnt, F, 3), device="cuda")
         flush = torch.empty(int(256 << 20) // 4, device="cuda")  # > 126 MB L2
         gathered = torch.empty((A, F, n), device="cuda") if strong else None
         gathered_raw = torch.empty((ws * a_cnt, F, n), device="cuda") if strong else None
-        feats = torch.empty((ws, 2, F), device="cuda") if (ws > 1 and not strong) else None
+        feats = torch.empty((ws * a_cnt, F, 3), device="cuda") if (ws > 1 and not strong) else None
     tex = None
     if args.sampler == 1:
         from paper_1604_03410_b200.trace import image_texture
         tex = image_texture(img.data_ptr(), n, sptr)
 
+    feats_on = wl["features"]
+    launches_per_step = 2 if feats_on else 1
+
     def step():
         tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
                         out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
                         pair_stride=pair)
+
+    def features():
+        if feats_on:  # P-functional (circus) stage consuming the sinograms
+            tt.circus_device(out.data_ptr(), n, a_cnt * F, circ.data_ptr(), stream=sptr)
 
     def exchange():
         if not dist:
@@ -212,13 +221,13 @@ def run_ours(args, ws, rank, local):
         with torch.cuda.stream(stream):
             if strong:  # the single NCCL gather of sinogram slices (equal shards: (A/2) % ws == 0)
                 shard.gather_sinograms(out, A, dist, out=gathered, raw=gathered_raw)
-            else:       # image-batch sharding: gather per-image feature summaries
-                f = torch.stack([out.sum(dim=(0, 2)), out.amax(dim=(0, 2))])
-                dist.all_gather_into_tensor(feats, f)
+            else:       # image-batch sharding: gather the per-image circus features
+                dist.all_gather_into_tensor(feats, circ)
 
     torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
+        features()
         exchange()
     torch.cuda.synchronize()
     if dist:
@@ -238,6 +247,7 @@ def run_ours(args, ws, rank, local):
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
+            features()
             exchange()
             ev[i][2].record(stream)
         torch.cuda.synchronize()
@@ -258,32 +268,35 @@ def run_ours(args, ws, rank, local):
     ctx = tt.create_context(local)
     ctx.set_sampler(args.sampler)
     # public API on this rank's share (contiguous angle block under torchrun c3)
-    tr = tt.TraceTransform(ctx, n, A, full=full, a0=rank * a_cnt if strong else 0, a_count=a_cnt)
+    tr = tt.TraceTransform(ctx, n, A, full=full, a0=rank * a_cnt if strong else 0, a_count=a_cnt,
+                           features=feats_on)
     from paper_1604_03410_b200._lib import lib
     import ctypes as C
-    nb_img, nb_out, nb_med = n * n * 4, a_cnt * F * n * 4, a_cnt * 2 * n * 4
-    hp = [C.c_void_p() for _ in range(3)]
-    for h, nb in zip(hp, (nb_img, nb_out, nb_med)):
+    nb_img, nb_out, nb_med, nb_circ = n * n * 4, a_cnt * F * n * 4, a_cnt * 2 * n * 4, a_cnt * F * 3 * 4
+    hp = [C.c_void_p() for _ in range(4)]
+    for h, nb in zip(hp, (nb_img, nb_out, nb_med, nb_circ)):
         assert lib.tt_host_alloc(nb, C.byref(h)) == 0
     h_img = np.ctypeslib.as_array((C.c_float * (n * n)).from_address(hp[0].value)).reshape(n, n)
     h_img[:] = img_h
     h_out = np.ctypeslib.as_array((C.c_float * (a_cnt * F * n)).from_address(hp[1].value))
     h_med = np.ctypeslib.as_array((C.c_int32 * (a_cnt * 2 * n)).from_address(hp[2].value))
+    h_circ = np.ctypeslib.as_array((C.c_float * (a_cnt * F * 3)).from_address(hp[3].value))
     for _ in range(max(2, args.warmup)):
-        tr.run_resident(h_img, h_out, h_med if full else None)
+        tr.run_resident(h_img, h_out, h_med if full else None, h_circ if feats_on else None)
     e2e_steps = max(5, min(args.steps, 50))
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        tr.run_resident(h_img, h_out, h_med if full else None)
+        tr.run_resident(h_img, h_out, h_med if full else None, h_circ if feats_on else None)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if dist:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": samples_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nb_img,
-           "d2h_bytes_per_step": nb_out + (nb_med if full else 0), "ms_per_step": e2e_s * 1e3,
+           "d2h_bytes_per_step": nb_out + (nb_med if full else 0) + (nb_circ if feats_on else 0),
+           "ms_per_step": e2e_s * 1e3,
            "api": "TraceTransform.run_resident -> tt_memcpy_htod / tt_launch(trace_t05) / tt_memcpy_dtoh"}
     # parity spot check of the e2e output against the device-resident one
     same = (not strong) and np.array_equal(h_out.reshape(a_cnt, F, n), out.cpu().numpy())
@@ -313,12 +326,13 @@ def run_ours(args, ws, rank, local):
             "scaling": "strong" if args.workload == "c3" else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (disk-masked U[0,1) noise, seed 20160412 + rank)",
             "config": {"workload": args.workload, "desc": wl["desc"], "image": [n, n], "angles": A,
-                       "functionals": "T0-T5" if full else "T0", "sampler": ["ldg", "tex"][args.sampler],
+                       "functionals": ("T0-T5" if full else "T0") + (" + P1-P3 circus" if feats_on else ""),
+                       "sampler": ["ldg", "tex"][args.sampler],
                        "parallelism": (f"orientations sharded x{ws} + NCCL all_gather" if strong else
                                        (f"images sharded x{ws} + NCCL feature gather" if ws > 1 else "1 GPU")),
                        "l2": "flushed (256 MiB memset) between timed steps", "ms_per_image": ms_per_step},
             "e2e": e2e, "roofline": roofline, "clocks": clocks.summary(),
-            "gpu_launches": args.steps * 1, "e2e_matches_device_result": bool(same)}
+            "gpu_launches": args.steps * launches_per_step, "e2e_matches_device_result": bool(same)}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl)
     if tex is not None:

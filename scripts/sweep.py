@@ -1,0 +1,81 @@
+"""Config C5 sweep (BASELINE.json configs[4]): n in 128..8192 x angles in
+180..2880, T0-only (Radon) vs T0-T5, one GPU.  Device-resident timing with
+CUDA events on the launch stream, L2 flushed before every timed launch.
+Prints one JSON line per point (ms, sinogram samples/s, taps/s, FLOP
+fraction of the measured FFMA peak).
+
+  python scripts/sweep.py [--quick] > profiles/sweep_rNN.jsonl
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1604_03410_b200 as tt  # noqa: E402
+from paper_1604_03410_b200._lib import lib  # noqa: E402
+from paper_1604_03410_b200.trace import image_texture, image_texture_destroy  # noqa: E402
+
+
+def run_point(n, A, full, stream, flush, reps, peak):
+    F = 6 if full else 1
+    c, s, w = tt.make_tables(n, A)
+    img = torch.from_numpy(tt.synth_image(tt.DISK, n)).cuda()
+    ct, st, wt = (torch.from_numpy(x).cuda() for x in (c, s, w))
+    out = torch.empty((A, F, n), device="cuda")
+    med = torch.empty((A, 2, n), dtype=torch.int32, device="cuda") if full else None
+    sp = stream.cuda_stream
+    tex = image_texture(img.data_ptr(), n, sp)
+
+    def launch():
+        tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
+                        med.data_ptr() if full else 0, full=full, sampler=1, stream=sp, tex=tex)
+
+    for _ in range(2):
+        launch()
+    times = []
+    for _ in range(reps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launch()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    image_texture_destroy(tex)
+    ms = sorted(times)[len(times) // 2]
+    taps = lib.tt_count_inbounds_taps(n, 0, A, c.ctypes.data, s.ctypes.data)
+    flops = bench.FLOPS_PER_TAP[full] * taps
+    return {"n": n, "angles": A, "functionals": "T0-T5" if full else "T0", "ms": ms,
+            "samples_per_s": F * A * n / (ms / 1e3), "taps_per_s": taps / (ms / 1e3),
+            "tflops": flops / (ms / 1e3) / 1e12, "fp32_frac": flops / (ms / 1e3) / 1e12 / peak}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    stream = torch.cuda.Stream()
+    flush = torch.empty(int(256 << 20) // 4, device="cuda")
+    peak = bench.fp32_peak_tflops(torch, tt, stream)
+    ns = [128, 256, 512, 1024, 2048, 4096, 8192]
+    angles = [180, 360, 720, 1440, 2880]
+    if args.quick:
+        ns, angles = [256, 1024, 4096], [360, 1440]
+    for n in ns:
+        for A in angles:
+            for full in (False, True):
+                if full and n > tt.max_full_n():
+                    continue
+                reps = 5 if n * n * A > 4e10 else 10
+                pt = run_point(n, A, full, stream, flush, reps, peak)
+                pt["fp32_peak_tflops"] = peak
+                print(json.dumps(pt), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -18,7 +18,7 @@ def ctx(gpu):
 
 
 def _check_against_truth(sino, circ):
-    rc, r64, _ = O.circus(sino)
+    rc, r64, rm = O.circus(sino)
     assert np.array_equal(circ.view(np.uint32), rc.view(np.uint32)), "differs bitwise from the replay"
     n = sino.shape[-1]
     chain = (n + 31) // 32 + 10
@@ -26,11 +26,16 @@ def _check_against_truth(sino, circ):
     p1_err = np.abs(circ[..., 0] - r64[..., 0]) / (1e-4 * np.abs(r64[..., 0]) + 1e-30 + eps * r64[..., 0])
     assert np.all(p1_err <= 1.0)
     assert np.array_equal(circ[..., 2], r64[..., 2].astype(np.float32))
-    rows = sino.reshape(-1, n)
-    flat = circ.reshape(-1, 3)
-    for i in range(rows.shape[0]):  # P2 is the value at an eps-median index
-        idx = np.nonzero(rows[i] == flat[i, 1])[0]
-        assert any(O.is_eps_median(rows[i], int(m), eps) for m in idx) or (flat[i, 1] == 0 and not rows[i].any())
+    # P2 = s[m] at the replayed (== GPU) median index m, which must be an eps-median of the f64 prefix
+    rows = sino.reshape(-1, n).astype(np.float64)
+    m = rm.reshape(-1).astype(np.int64)
+    P = np.cumsum(rows, axis=1)
+    S = P[:, -1]
+    Pm = np.take_along_axis(P, m[:, None], 1)[:, 0]
+    Pprev = np.where(m > 0, np.take_along_axis(P, np.maximum(m - 1, 0)[:, None], 1)[:, 0], 0.0)
+    ok = np.where(S > 0, (2 * Pm >= S * (1 - eps)) & ((m == 0) | (2 * Pprev < S * (1 + eps))), m == 0)
+    assert ok.all()
+    assert np.array_equal(circ.reshape(-1, 3)[:, 1], sino.reshape(-1, n)[np.arange(m.size), m])
 
 
 @pytest.mark.parametrize("n,A,kind", [(64, 10, tt.DISK), (256, 360, tt.PHANTOM), (1000, 8, tt.SPARSE),
