@@ -39,6 +39,8 @@ WORKLOADS = {
     "c2": dict(n=1024, angles=720, full=True, features=True,
                desc="1024^2 fp32, 720 angles x 1024 lines, T0-T5 + P-functionals (circus)"),
     "c3": dict(n=4096, angles=1440, full=True, features=False, desc="4096^2 fp32, 1440 angles x 4096 lines, T0-T5"),
+    "c4": dict(n=256, angles=360, full=True, features=True, batch=4096,
+               desc="batched feature extraction: 4096 x 256^2 fp32, 360 angles, T0-T5 + circus"),
 }
 FLOPS_PER_TAP = {True: 34, False: 16}  # FMA = 2, in-bounds taps only
 METRIC = "trace-transform sinogram samples/s"
@@ -133,37 +135,54 @@ def load_traffic(workload: str):
         return None, None
 
 
-def cpu_baseline(wl, seconds_target=12.0):
-    """The oracle port (TTO_SEQ32, OpenMP over lines, all host threads) on a
-    bounded sample of angles of the same workload."""
-    import numpy as np
-
+def cpu_baseline(wl, seconds_target=10.0):
+    """The oracle port (TTO_SEQ32 sampler + functionals, and the circus stage
+    when the workload has it; OpenMP over lines on all host threads) on a
+    bounded sample of the same workload: whole images repeated (or a prefix of
+    the angles) until about `seconds_target` of CPU work."""
     import oracle as O
     import paper_1604_03410_b200 as tt
     n, A = wl["n"], wl["angles"]
     img = tt.synth_image(tt.DISK, n)
     c, s, w = tt.make_tables(n, A)
     cores = os.cpu_count() or 1
+
+    def run(a_count):
+        out, _, _, _ = O.transform(img, n, c, s, w, a0=0, a_count=a_count, mode=O.SEQ32, nthreads=cores)
+        if wl.get("features"):
+            O.circus(out, nthreads=cores)
+
     a_count, t = 1, 0.0
     while True:
         t0 = time.perf_counter()
-        O.transform(img, n, c, s, w, a0=0, a_count=a_count, mode=O.SEQ32, nthreads=cores)
+        run(a_count)
         t = time.perf_counter() - t0
         if t >= seconds_target / 4 or a_count >= A:
             break
         a_count = min(A, max(a_count * 2, int(a_count * seconds_target / 4 / max(t, 1e-3))))
-    samples = 6 * a_count * n
+    reps = max(1, int(seconds_target / max(t, 1e-3)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        run(a_count)
+    t = time.perf_counter() - t0
+    samples = 6 * a_count * n * reps
     return {"value": samples / t, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"oracle TTO_SEQ32 (sequential fp32, pinned sampler) on {a_count} of {A} angles x {n} "
-                      f"lines of the {wl['desc']} workload, {t:.2f} s wall, OpenMP {cores} threads",
+            "sample": f"oracle TTO_SEQ32 (sequential fp32, pinned sampler){' + circus' if wl.get('features') else ''}"
+                      f" on {a_count} of {A} angles x {n} lines of one {n}^2 image, repeated {reps}x "
+                      f"({t:.1f} s wall, OpenMP {cores} threads)",
             "seconds": t}
 
 
 def run_ours(args, ws, rank, local):
+    import ctypes as C
+
     import numpy as np
     import torch
 
     import paper_1604_03410_b200 as tt
+    from paper_1604_03410_b200 import shard
+    from paper_1604_03410_b200._lib import lib
+    from paper_1604_03410_b200.trace import image_atlas, image_texture, image_texture_destroy, image_texture_update
 
     torch.cuda.set_device(local)
     dist = None
@@ -171,57 +190,61 @@ def run_ours(args, ws, rank, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = WORKLOADS[args.workload]
-    n, A, full = wl["n"], wl["angles"], wl["full"]
+    n, A, full, feats_on = wl["n"], wl["angles"], wl["full"], wl["features"]
     F = 6 if full else 1
-    strong = args.workload == "c3" and ws > 1
-    # Orientation shards keep the mirror pairing: rank r owns
-    # angles [a0, a0+cnt) and [A/2+a0, A/2+a0+cnt) -> rows [cnt] + [cnt].
+    batch_total = wl.get("batch", 1)
+    orient = args.workload == "c3" and ws > 1        # orientation shards + sinogram gather (strong)
+    images = batch_total > 1                         # image shards (strong over a fixed batch)
     h = A // 2
-    if strong:
-        from paper_1604_03410_b200 import shard
+    if orient:
+        # rank r owns angles [a0, a0+cnt) and their mirrors [A/2+a0, ...) -> rows [cnt] + [cnt]
         a0, cnt, pair = shard.orientation_shard(A, ws, rank)
         a_cnt = 2 * cnt
     else:
         a0, a_cnt, pair = 0, A, 0
+    if images:
+        b0, B = shard.image_shard(batch_total, ws, rank)
+    else:
+        b0, B = rank, 1  # c1/c2 under torchrun: one image per rank (weak scaling)
 
     stream = torch.cuda.Stream()
     sptr = stream.cuda_stream
     ctab_h, stab_h, wtab_h = tt.make_tables(n, A)
-    img_h = tt.synth_image(tt.DISK, n, tt.SEEDS[tt.DISK] + (0 if strong else rank))
+    seed0 = tt.SEEDS[tt.DISK]
+    img_h = np.stack([tt.synth_image(tt.DISK, n, seed0 + (0 if orient else b0 + b)) for b in range(B)])
     with torch.cuda.stream(stream):
         img = torch.from_numpy(img_h).cuda()
         ctab, stab, wtab = (torch.from_numpy(x).cuda() for x in (ctab_h, stab_h, wtab_h))
-        out = torch.empty((a_cnt, F, n), device="cuda")
-        med = torch.empty((a_cnt, 2, n), dtype=torch.int32, device="cuda")
-        circ = torch.empty((a_cnt, F, 3), device="cuda")
+        out = torch.empty((B, a_cnt, F, n), device="cuda")
+        med = torch.empty((B, a_cnt, 2, n), dtype=torch.int32, device="cuda")
+        circ = torch.empty((B, a_cnt, F, 3), device="cuda")
         flush = torch.empty(int(256 << 20) // 4, device="cuda")  # > 126 MB L2
-        gathered = torch.empty((A, F, n), device="cuda") if strong else None
-        gathered_raw = torch.empty((ws * a_cnt, F, n), device="cuda") if strong else None
-        feats = torch.empty((ws * a_cnt, F, 3), device="cuda") if (ws > 1 and not strong) else None
+        gathered = torch.empty((A, F, n), device="cuda") if orient else None
+        gathered_raw = torch.empty((ws * a_cnt, F, n), device="cuda") if orient else None
+        feats = torch.empty((ws * B, a_cnt, F, 3), device="cuda") if (ws > 1 and not orient) else None
     tex = None
-    if args.sampler == 1:
-        from paper_1604_03410_b200.trace import image_texture
-        tex = image_texture(img.data_ptr(), n, sptr)
-
-    feats_on = wl["features"]
-    launches_per_step = 2 if feats_on else 1
+    if args.sampler == 1:  # texture layout of this step's image(s); refreshed inside every timed step
+        tex = image_atlas(img.data_ptr(), n, B, 0, sptr) if B > 1 else image_texture(img.data_ptr(), n, sptr)
+    launches_per_step = 1 + (1 if feats_on else 0) + (1 if tex is not None and B > 1 else 0)
 
     def step():
+        if tex is not None:
+            image_texture_update(tex, img.data_ptr(), 0, sptr)
         tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
                         out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
-                        pair_stride=pair)
+                        pair_stride=pair, batch=B)
 
     def features():
         if feats_on:  # P-functional (circus) stage consuming the sinograms
-            tt.circus_device(out.data_ptr(), n, a_cnt * F, circ.data_ptr(), stream=sptr)
+            tt.circus_device(out.data_ptr(), n, B * a_cnt * F, circ.data_ptr(), stream=sptr)
 
     def exchange():
         if not dist:
             return
         with torch.cuda.stream(stream):
-            if strong:  # the single NCCL gather of sinogram slices (equal shards: (A/2) % ws == 0)
-                shard.gather_sinograms(out, A, dist, out=gathered, raw=gathered_raw)
-            else:       # image-batch sharding: gather the per-image circus features
+            if orient:  # the single NCCL gather of sinogram slices (equal shards: (A/2) % ws == 0)
+                shard.gather_sinograms(out[0], A, dist, out=gathered, raw=gathered_raw)
+            else:       # image sharding: gather the per-image circus features
                 dist.all_gather_into_tensor(feats, circ)
 
     torch.cuda.synchronize()
@@ -234,8 +257,8 @@ def run_ours(args, ws, rank, local):
         dist.barrier()
 
     # ---- timed region (device events per step; L2 flushed between steps) ----
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local)
     with clocks:
         torch.cuda.synchronize()
@@ -261,54 +284,68 @@ def run_ours(args, ws, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    samples_step = F * A * n * (1 if strong else ws)  # whole job per step
+    if orient:
+        samples_step = F * A * n                     # one image, angles split over ranks
+    elif images:
+        samples_step = F * A * n * batch_total       # the whole batch, images split over ranks
+    else:
+        samples_step = F * A * n * ws                # one image per rank
     value = samples_step / (ms_per_step / 1e3)
 
     # ---- e2e through the public API (host buffers, copies in the timed region) ----
     ctx = tt.create_context(local)
     ctx.set_sampler(args.sampler)
     # public API on this rank's share (contiguous angle block under torchrun c3)
-    tr = tt.TraceTransform(ctx, n, A, full=full, a0=rank * a_cnt if strong else 0, a_count=a_cnt,
-                           features=feats_on)
-    from paper_1604_03410_b200._lib import lib
-    import ctypes as C
-    nb_img, nb_out, nb_med, nb_circ = n * n * 4, a_cnt * F * n * 4, a_cnt * 2 * n * 4, a_cnt * F * 3 * 4
+    tr = tt.TraceTransform(ctx, n, A, full=full, a0=rank * a_cnt if orient else 0, a_count=a_cnt,
+                           features=feats_on, batch=B)
+    nb_img, nb_out = B * n * n * 4, B * a_cnt * F * n * 4
+    nb_med, nb_circ = B * a_cnt * 2 * n * 4, B * a_cnt * F * 3 * 4
+    # feature extraction (c4) returns the features; the sinogram workloads return sinograms + medians
+    want_sino = not images
     hp = [C.c_void_p() for _ in range(4)]
-    for h, nb in zip(hp, (nb_img, nb_out, nb_med, nb_circ)):
-        assert lib.tt_host_alloc(nb, C.byref(h)) == 0
-    h_img = np.ctypeslib.as_array((C.c_float * (n * n)).from_address(hp[0].value)).reshape(n, n)
+    for hh, nb in zip(hp, (nb_img, nb_out if want_sino else 4, nb_med if want_sino else 4, nb_circ)):
+        assert lib.tt_host_alloc(nb, C.byref(hh)) == 0
+    h_img = np.ctypeslib.as_array((C.c_float * (B * n * n)).from_address(hp[0].value)).reshape(img_h.shape)
     h_img[:] = img_h
-    h_out = np.ctypeslib.as_array((C.c_float * (a_cnt * F * n)).from_address(hp[1].value))
-    h_med = np.ctypeslib.as_array((C.c_int32 * (a_cnt * 2 * n)).from_address(hp[2].value))
-    h_circ = np.ctypeslib.as_array((C.c_float * (a_cnt * F * 3)).from_address(hp[3].value))
-    for _ in range(max(2, args.warmup)):
-        tr.run_resident(h_img, h_out, h_med if full else None, h_circ if feats_on else None)
-    e2e_steps = max(5, min(args.steps, 50))
+    h_out = np.ctypeslib.as_array((C.c_float * (nb_out // 4)).from_address(hp[1].value)) if want_sino else None
+    h_med = np.ctypeslib.as_array((C.c_int32 * (nb_med // 4)).from_address(hp[2].value)) if want_sino else None
+    h_circ = np.ctypeslib.as_array((C.c_float * (nb_circ // 4)).from_address(hp[3].value))
+    img_arg = h_img if B > 1 else h_img[0]
+    for _ in range(max(2, min(args.warmup, 3) if images else args.warmup)):
+        tr.run_resident(img_arg, h_out, h_med if full else None, h_circ if feats_on else None)
+    e2e_steps = max(3, min(args.steps, 5 if images else 50))
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        tr.run_resident(h_img, h_out, h_med if full else None, h_circ if feats_on else None)
+        tr.run_resident(img_arg, h_out, h_med if full else None, h_circ if feats_on else None)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if dist:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": samples_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nb_img,
-           "d2h_bytes_per_step": nb_out + (nb_med if full else 0) + (nb_circ if feats_on else 0),
+    d2h = (nb_out + (nb_med if full else 0) if want_sino else 0) + (nb_circ if feats_on else 0)
+    e2e = {"value": samples_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nb_img, "d2h_bytes_per_step": d2h,
            "ms_per_step": e2e_s * 1e3,
-           "api": "TraceTransform.run_resident -> tt_memcpy_htod / tt_launch(trace_t05) / tt_memcpy_dtoh"}
+           "api": ("TraceTransform.run_resident -> tt_memcpy_htod / tt_launch(" +
+                   ("trace_t05_batch" if B > 1 else "trace_t05") + (", circus" if feats_on else "") +
+                   ") / tt_memcpy_dtoh")}
     # parity spot check of the e2e output against the device-resident one
-    same = (not strong) and np.array_equal(h_out.reshape(a_cnt, F, n), out.cpu().numpy())
+    if want_sino and not orient:
+        same = np.array_equal(h_out.reshape(out.shape), out.cpu().numpy())
+    else:
+        same = np.array_equal(h_circ.reshape(circ.shape), circ.cpu().numpy())
     tr.free_resident()
     ctx.destroy()
-    for h in hp:
-        lib.tt_host_free(h)
+    for hh in hp:
+        lib.tt_host_free(hh)
 
-    # ---- roofline of the fused kernel (rank 0's shard) ----
-    taps = lib.tt_count_inbounds_taps(n, a0, a_cnt // 2, ctab_h.ctypes.data, stab_h.ctypes.data) + \
-        lib.tt_count_inbounds_taps(n, a0 + h, a_cnt // 2, ctab_h.ctypes.data, stab_h.ctypes.data) if strong else \
-        lib.tt_count_inbounds_taps(n, 0, A, ctab_h.ctypes.data, stab_h.ctypes.data)
+    # ---- roofline of the fused kernel (this rank's launch) ----
+    if orient:
+        taps = lib.tt_count_inbounds_taps(n, a0, cnt, ctab_h.ctypes.data, stab_h.ctypes.data) + \
+            lib.tt_count_inbounds_taps(n, a0 + h, cnt, ctab_h.ctypes.data, stab_h.ctypes.data)
+    else:
+        taps = B * lib.tt_count_inbounds_taps(n, 0, A, ctab_h.ctypes.data, stab_h.ctypes.data)
     kern_s = statistics.mean(kern_ms) / 1e3
     peak = fp32_peak_tflops(torch, tt, stream)
     achieved = FLOPS_PER_TAP[full] * taps / kern_s / 1e12
@@ -319,24 +356,26 @@ def run_ours(args, ws, rank, local):
                                "FP32 is the bound (image L2-resident; no tensor-core work)",
                 "work": f"{FLOPS_PER_TAP[full]} flop per in-bounds tap x {taps} taps (SURVEY.md 8d)",
                 "kernel_ms": kern_s * 1e3, "taps_per_s": taps / kern_s,
-                "hbm_algorithmic_bytes": n * n * 4 + a_cnt * (F + 2) * n * 4,
+                "hbm_algorithmic_bytes": B * (n * n * 4 + a_cnt * (F + 2) * n * 4),
                 "traffic_source": traffic_src}
+    scaling = "strong" if (orient or images) else "weak"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if args.workload == "c3" else "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (disk-masked U[0,1) noise, seed 20160412 + rank)",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (disk-masked U[0,1) noise, seed 20160412 + image index)",
             "config": {"workload": args.workload, "desc": wl["desc"], "image": [n, n], "angles": A,
+                       "images": batch_total if images else (1 if orient else ws),
                        "functionals": ("T0-T5" if full else "T0") + (" + P1-P3 circus" if feats_on else ""),
                        "sampler": ["ldg", "tex"][args.sampler],
-                       "parallelism": (f"orientations sharded x{ws} + NCCL all_gather" if strong else
+                       "parallelism": (f"orientations sharded x{ws} + NCCL all_gather" if orient else
                                        (f"images sharded x{ws} + NCCL feature gather" if ws > 1 else "1 GPU")),
-                       "l2": "flushed (256 MiB memset) between timed steps", "ms_per_image": ms_per_step},
+                       "l2": "flushed (256 MiB memset) between timed steps",
+                       "ms_per_image": ms_per_step / (batch_total if images else 1)},
             "e2e": e2e, "roofline": roofline, "clocks": clocks.summary(),
             "gpu_launches": args.steps * launches_per_step, "e2e_matches_device_result": bool(same)}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl)
     if tex is not None:
-        from paper_1604_03410_b200.trace import image_texture_destroy
         image_texture_destroy(tex)
     if dist:
         dist.destroy_process_group()

@@ -238,6 +238,10 @@ typedef struct tt_trace_desc {
     int32_t* med;
     int32_t sampler;
     int32_t pair_stride;
+    int32_t batch;      /* images (0 or 1: one); image b at img + b*img_stride, outputs
+                           at out + b*rows*F*n and med + b*rows*2*n (rows = a_count) */
+    int32_t _pad2;
+    int64_t img_stride; /* elements between images (0: n*n) */
 } tt_trace_desc;
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
 
@@ -250,6 +254,12 @@ tt_status tt_circus_device(const float* d_sino, int n, int rows, float* d_circ, 
  * (sampler 1 without the per-call copy). */
 typedef struct tt_image_tex tt_image_tex;
 tt_status tt_image_tex_create(const float* d_img, int n, void* stream, tt_image_tex** out);
+/* Texture atlas of a batch of n x n images (image b at d_imgs + b*img_stride)
+ * for batched tt_trace_device_tex calls (batched feature extraction). */
+tt_status tt_image_atlas_create(const float* d_imgs, int n, int batch, int64_t img_stride, void* stream,
+                                tt_image_tex** out);
+/* Re-copy the image(s) into an existing texture/atlas (stream-ordered). */
+tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, int64_t img_stride, void* stream);
 tt_status tt_image_tex_destroy(tt_image_tex* t);
 tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, void* stream);
 

@@ -6,7 +6,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtt_b200.so")
+LIB_PATH = os.environ.get("TT_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtt_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1604_03410_b200.build` "
@@ -51,7 +51,8 @@ class Counters(C.Structure):
 class TraceDesc(C.Structure):
     _fields_ = [("img", C.c_void_p), ("n", C.c_int32), ("a0", C.c_int32), ("a_count", C.c_int32),
                 ("full", C.c_int32), ("ctab", C.c_void_p), ("stab", C.c_void_p), ("wtab", C.c_void_p),
-                ("out", C.c_void_p), ("med", C.c_void_p), ("sampler", C.c_int32), ("pair_stride", C.c_int32)]
+                ("out", C.c_void_p), ("med", C.c_void_p), ("sampler", C.c_int32), ("pair_stride", C.c_int32),
+                ("batch", C.c_int32), ("_pad2", C.c_int32), ("img_stride", C.c_int64)]
 
 
 ARG_I32, ARG_I64, ARG_F32, ARG_F64, ARG_PTR = range(5)
@@ -95,6 +96,8 @@ _sigs = {
     "tt_trace_device": (_S, [C.POINTER(TraceDesc), C.c_void_p]),
     "tt_circus_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_image_tex_create": (_S, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "tt_image_atlas_create": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "tt_image_tex_update": (_S, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "tt_image_tex_destroy": (_S, [C.c_void_p]),
     "tt_trace_device_tex": (_S, [C.POINTER(TraceDesc), C.c_void_p, C.c_void_p]),
 }

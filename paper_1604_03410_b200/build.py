@@ -29,17 +29,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libtt_b200.so (or a variant with extra -D flags into `out`, for experiments)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     cmd = ["nvcc", "-ccbin", "g++", "-shared", "-Xcompiler", "-fPIC,-ffp-contract=off", *ARCH, "-O3",
-           "-lineinfo", "-std=c++17", "-I" + os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB + ".tmp"]
+           "-lineinfo", "-std=c++17", "-I" + os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines],
+           *[os.path.join(CSRC, f) for f in SOURCES], "-o", target + ".tmp"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

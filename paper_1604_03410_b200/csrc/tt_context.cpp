@@ -113,6 +113,8 @@ struct Alloc {
 struct TexEntry {
     std::uint64_t gen = ~0ull;
     int n = 0;
+    int batch = 1;
+    int cols = 1;
     cudaArray_t arr = nullptr;
     cudaTextureObject_t tex = 0;
 };
@@ -458,10 +460,15 @@ LaunchOutcome run_add_to(tt_ctx& ctx, const tt_grid& g, const std::vector<Resolv
 // kernel oracle/trace_t05.krn computes p = (block_y-1)*threads_x + thread_x-1).
 LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg& img, int n, const ResolvedArg& ct,
                                const ResolvedArg& st, const ResolvedArg* wt, const ResolvedArg& out,
-                               const ResolvedArg* med, int a0, bool full) {
+                               const ResolvedArg* med, int a0, bool full, int batch = 1) {
     LaunchOutcome o;
     const std::int64_t a_count = g.grid[0];
-    if (n <= 0) return o;  // every thread fails `p < n`: no work
+    if (n <= 0 || batch <= 0) return o;  // every thread fails `p < n` (or no image): no work
+    if (batch > 1 && std::uint64_t(g.grid[2]) < std::uint64_t(batch)) {
+        o.status = TT_ERR_LAUNCH_CONFIG;
+        o.error = "LaunchConfigError: trace_t05_batch requires grid.z >= batch (one z-slice per image)";
+        return o;
+    }
     if (std::uint64_t(g.grid[1]) * g.block[0] < std::uint64_t(n)) {
         o.status = TT_ERR_LAUNCH_CONFIG;
         o.error = "LaunchConfigError: native trace kernels require grid.y*block.x >= n (every line covered)";
@@ -475,10 +482,11 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     }
     const std::uint64_t N = std::uint64_t(n);
     const std::int64_t F = full ? tt::kNumF : 1;
-    bool oob = a0 < 0 || elems(img, 4) < N * N || std::int64_t(elems(ct, 4)) < a0 + a_count ||
-               std::int64_t(elems(st, 4)) < a0 + a_count || elems(out, 4) < std::uint64_t(a_count * F) * N;
+    const std::uint64_t B = std::uint64_t(batch);
+    bool oob = a0 < 0 || elems(img, 4) < B * N * N || std::int64_t(elems(ct, 4)) < a0 + a_count ||
+               std::int64_t(elems(st, 4)) < a0 + a_count || elems(out, 4) < B * std::uint64_t(a_count * F) * N;
     if (wt) oob = oob || elems(*wt, 4) < 8 * N;
-    if (med) oob = oob || elems(*med, 4) < std::uint64_t(a_count) * 2 * N;
+    if (med) oob = oob || elems(*med, 4) < B * std::uint64_t(a_count) * 2 * N;
     if (oob) {
         o.trap = first_thread_trap(TT_TRAP_GLOBAL_OUT_OF_BOUNDS);
         return o;
@@ -494,29 +502,37 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     ta.out = (float*)out.dptr;
     ta.med = med ? (std::int32_t*)med->dptr : nullptr;
     ta.full = full;
+    ta.batch = batch;
     ta.sampler = tt::Sampler(ctx.sampler);
     if (ta.sampler == tt::Sampler::Texture) {
         TexEntry& te = ctx.tex_cache[img.base];
-        if (te.arr == nullptr || te.n != n) {
+        if (te.arr == nullptr || te.n != n || te.batch != batch) {
             if (te.arr) {
                 cudaStreamSynchronize(ctx.stream);
                 cudaDestroyTextureObject(te.tex);
                 cudaFreeArray(te.arr);
                 te = TexEntry{};
             }
-            cudaError_t e = tt::make_image_texture(ta.img, n, ctx.stream, &te.arr, &te.tex);
+            cudaError_t e = batch > 1 ? tt::make_image_atlas(ta.img, n, batch, (long long)N * N, ctx.stream, &te.arr,
+                                                              &te.tex, &te.cols)
+                                      : tt::make_image_texture(ta.img, n, ctx.stream, &te.arr, &te.tex);
             if (e != cudaSuccess) {
                 ctx.tex_cache.erase(img.base);
-                return cuda_outcome(e, "make_image_texture");
+                return cuda_outcome(e, "image texture");
             }
             te.n = n;
+            te.batch = batch;
             te.gen = img.gen;
         } else if (te.gen != img.gen) {  // image rewritten since the copy: refresh (stream-ordered)
-            cudaError_t e = cudaMemcpy2DToArrayAsync(te.arr, 0, 0, ta.img, std::size_t(n) * 4, std::size_t(n) * 4,
-                                                     std::size_t(n), cudaMemcpyDeviceToDevice, ctx.stream);
+            cudaError_t e = batch > 1 ? tt::fill_image_atlas(te.arr, ta.img, n, batch, (long long)N * N, te.cols,
+                                                              ctx.stream)
+                                      : cudaMemcpy2DToArrayAsync(te.arr, 0, 0, ta.img, std::size_t(n) * 4,
+                                                                 std::size_t(n) * 4, std::size_t(n),
+                                                                 cudaMemcpyDeviceToDevice, ctx.stream);
             if (e != cudaSuccess) return cuda_outcome(e, "texture refresh");
             te.gen = img.gen;
         }
+        ta.atlas_cols = te.cols;
         ta.tex = te.tex;
     }
     o = cuda_outcome(tt::launch_trace(ta, ctx.stream), "trace kernel");
@@ -528,6 +544,14 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
 // DSL kernel oracle/trace_t05.krn, bound to the fused sm_100a kernel.
 LaunchOutcome run_trace_t05(tt_ctx& ctx, const tt_grid& g, const std::vector<ResolvedArg>& a) {
     return run_trace_common(ctx, g, a[0], a[1].value.v.i32, a[2], a[3], &a[4], a[5], &a[6], a[7].value.v.i32, true);
+}
+
+// trace_t05_batch(img, n, ctab, stab, wtab, out, med, a0, batch): the same
+// kernel over `batch` images stacked [batch][n][n] (outputs stacked per image;
+// logical grid.z = batch) -- batched feature extraction (config C4).
+LaunchOutcome run_trace_t05_batch(tt_ctx& ctx, const tt_grid& g, const std::vector<ResolvedArg>& a) {
+    return run_trace_common(ctx, g, a[0], a[1].value.v.i32, a[2], a[3], &a[4], a[5], &a[6], a[7].value.v.i32, true,
+                            a[8].value.v.i32);
 }
 
 // radon(img, n, ctab, stab, out, a0): T0 only (SURVEY.md Appendix B's kernel
@@ -575,6 +599,10 @@ const std::vector<NativeKernel>& registry() {
             {P(true, f, "img"), P(false, i, "n"), P(true, f, "ctab"), P(true, f, "stab"), P(true, f, "wtab"),
              P(true, f, "out", true), P(true, i, "med", true), P(false, i, "a0")},
             run_trace_t05);
+        add("trace_t05_batch",
+            {P(true, f, "img"), P(false, i, "n"), P(true, f, "ctab"), P(true, f, "stab"), P(true, f, "wtab"),
+             P(true, f, "out", true), P(true, i, "med", true), P(false, i, "a0"), P(false, i, "batch")},
+            run_trace_t05_batch);
         add("radon",
             {P(true, f, "img"), P(false, i, "n"), P(true, f, "ctab"), P(true, f, "stab"), P(true, f, "out", true),
              P(false, i, "a0")},
@@ -1036,6 +1064,9 @@ static tt_status check_desc(const tt_trace_desc* d) {
     if (d->pair_stride > 0 && d->a_count % 2 != 0)
         return fail(nullptr, TT_ERR_INVALID, "explicit pair_stride needs an even a_count");
     if ((long long)d->a_count * d->n >= (1ll << 31)) return fail(nullptr, TT_ERR_INVALID, "launch too large");
+    if (d->batch < 0 || d->img_stride < 0) return fail(nullptr, TT_ERR_INVALID, "negative batch or stride");
+    if (d->img_stride != 0 && d->img_stride < (long long)d->n * d->n)
+        return fail(nullptr, TT_ERR_INVALID, "img_stride smaller than one image");
     if (!d->ctab || !d->stab || !d->out || (d->full && !d->wtab))
         return fail(nullptr, TT_ERR_INVALID, "null table or output pointer");
     if (d->full && (reinterpret_cast<std::uintptr_t>(d->wtab) & 15u))
@@ -1063,6 +1094,8 @@ static tt::TraceArgs to_args(const tt_trace_desc* d) {
     ta.out = d->out;
     ta.med = d->med;
     ta.full = d->full != 0;
+    ta.batch = d->batch > 1 ? d->batch : 1;
+    ta.img_stride = d->img_stride;
     return ta;
 }
 
@@ -1075,8 +1108,12 @@ tt_status tt_trace_device(const tt_trace_desc* d, void* stream) {
     if (d->sampler == 1) {
         cudaArray_t arr = nullptr;
         ta.sampler = tt::Sampler::Texture;
-        cudaError_t e = tt::make_image_texture(ta.img, ta.n, s, &arr, &ta.tex);
-        if (e != cudaSuccess) return cuda_fail(nullptr, e, "make_image_texture");
+        cudaError_t e = ta.batch > 1
+                            ? tt::make_image_atlas(ta.img, ta.n, ta.batch, ta.img_stride > 0 ? ta.img_stride
+                                                                                           : (long long)ta.n * ta.n,
+                                                   s, &arr, &ta.tex, &ta.atlas_cols)
+                            : tt::make_image_texture(ta.img, ta.n, s, &arr, &ta.tex);
+        if (e != cudaSuccess) return cuda_fail(nullptr, e, "image texture");
         e = tt::launch_trace(ta, s);
         cudaStreamSynchronize(s);
         cudaDestroyTextureObject(ta.tex);
@@ -1093,6 +1130,8 @@ struct tt_image_tex {
     cudaArray_t arr = nullptr;
     cudaTextureObject_t tex = 0;
     int n = 0;
+    int batch = 1;
+    int cols = 1;
 };
 
 extern "C" {
@@ -1116,6 +1155,34 @@ tt_status tt_image_tex_create(const float* d_img, int n, void* stream, tt_image_
     return TT_OK;
 }
 
+tt_status tt_image_atlas_create(const float* d_imgs, int n, int batch, std::int64_t img_stride, void* stream,
+                                tt_image_tex** out) {
+    if (!d_imgs || !out || n < 1 || batch < 1) return fail(nullptr, TT_ERR_INVALID, "bad argument");
+    auto t = std::make_unique<tt_image_tex>();
+    t->n = n;
+    t->batch = batch;
+    cudaError_t e = tt::make_image_atlas(d_imgs, n, batch, img_stride > 0 ? img_stride : (long long)n * n,
+                                         (cudaStream_t)stream, &t->arr, &t->tex, &t->cols);
+    if (e != cudaSuccess) {
+        if (t->arr) cudaFreeArray(t->arr);
+        return cuda_fail(nullptr, e, "make_image_atlas (batch too large for one 2-D texture?)");
+    }
+    *out = t.release();
+    return TT_OK;
+}
+
+tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, std::int64_t img_stride, void* stream) {
+    if (!t || !d_imgs) return fail(nullptr, TT_ERR_INVALID, "bad argument");
+    const long long stride = img_stride > 0 ? img_stride : (long long)t->n * t->n;
+    cudaError_t e;
+    if (t->batch == 1 && t->cols == 1)
+        e = cudaMemcpy2DToArrayAsync(t->arr, 0, 0, d_imgs, std::size_t(t->n) * 4, std::size_t(t->n) * 4,
+                                     std::size_t(t->n), cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    else
+        e = tt::fill_image_atlas(t->arr, d_imgs, t->n, t->batch, stride, t->cols, (cudaStream_t)stream);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "image texture update");
+}
+
 tt_status tt_image_tex_destroy(tt_image_tex* t) {
     if (!t) return TT_OK;
     cudaDestroyTextureObject(t->tex);
@@ -1129,8 +1196,10 @@ tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, voi
     if (st != TT_OK) return st;
     if (!t || t->n != d->n) return fail(nullptr, TT_ERR_INVALID, "texture does not match n");
     tt::TraceArgs ta = to_args(d);
+    if (ta.batch > t->batch) return fail(nullptr, TT_ERR_INVALID, "batch larger than the texture atlas");
     ta.sampler = tt::Sampler::Texture;
     ta.tex = t->tex;
+    ta.atlas_cols = t->cols;
     cudaError_t e = tt::launch_trace(ta, (cudaStream_t)stream);
     return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "trace kernel");
 }

@@ -35,6 +35,9 @@ struct TraceArgs {
     int32_t* med = nullptr;       // full: [rows][2][n] (m, m'), may be null
     bool full = true;             // T0..T5 (else T0 / Radon only)
     Sampler sampler = Sampler::Global;
+    int batch = 1;                // images in this launch (same n, same angles)
+    long long img_stride = 0;     // elements between images (0: n*n) -- Global sampler
+    int atlas_cols = 1;           // texture atlas tiles per row -- Texture sampler
 };
 
 // Warps per line of the fused kernel for side n — part of the reduction
@@ -88,6 +91,15 @@ cudaError_t launch_ffma_probe(float* out, int blocks, int iters, cudaStream_t s)
 // circ[row][3] = (P1 total variation, P2 weighted-median value, P3 max),
 // DESIGN.md §2.7.  One warp per row.
 cudaError_t launch_circus(const float* sino, int n, int rows, float* circ, cudaStream_t s);
+
+// Texture atlas of `batch` images (image b at tile (b % cols, b / cols)),
+// 32-bit texels holding the float bits.
+cudaError_t make_image_atlas(const float* imgs, int n, int batch, long long stride, cudaStream_t s, cudaArray_t* arr,
+                             cudaTextureObject_t* tex, int* cols);
+
+// Refill an atlas created by make_image_atlas (stream-ordered).
+cudaError_t fill_image_atlas(cudaArray_t arr, const float* imgs, int n, int batch, long long stride, int cols,
+                             cudaStream_t s);
 
 // Writes a buffer larger than L2 (timing hygiene between bench iterations).
 cudaError_t launch_l2_flush(void* buf, uint64_t bytes, cudaStream_t s);

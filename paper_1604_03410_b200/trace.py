@@ -23,6 +23,7 @@ NF = 6
 
 TRACE_T05 = KernelAst("trace_t05", ["img", "n", "ctab", "stab", "wtab", "out", "med", "a0"])
 CIRCUS = KernelAst("circus", ["sino", "n", "rows", "circ"])
+TRACE_T05_BATCH = KernelAst("trace_t05_batch", ["img", "n", "ctab", "stab", "wtab", "out", "med", "a0", "batch"])
 RADON = KernelAst("radon", ["img", "n", "ctab", "stab", "out", "a0"])
 
 
@@ -49,9 +50,9 @@ def max_full_n() -> int:
     return lib.tt_max_full_n()
 
 
-def launch_config(n: int, angles: int, block: int = 256) -> GridConfig:
+def launch_config(n: int, angles: int, block: int = 256, batch: int = 1) -> GridConfig:
     b = min(block, max(n, 1))
-    return GridConfig((angles, (n + b - 1) // b, 1), (b, 1, 1))
+    return GridConfig((angles, (n + b - 1) // b, batch), (b, 1, 1))
 
 
 class TraceTransform:
@@ -63,23 +64,38 @@ class TraceTransform:
     image in and the sinograms out (the e2e benchmark path)."""
 
     def __init__(self, ctx: DeviceContext, n: int, angles: int, full: bool = True, a0: int = 0,
-                 a_count: int | None = None, features: bool = False):
+                 a_count: int | None = None, features: bool = False, batch: int = 1):
         self.ctx, self.n, self.angles, self.full = ctx, n, angles, full
         self.features = features and full  # P-functional (circus) stage after the trace kernel
         self.a0 = a0
         self.a_count = angles - a0 if a_count is None else a_count
+        self.batch = batch  # > 1: trace_t05_batch over [batch][n][n] images (T0-T5 only)
+        if batch > 1 and not full:
+            raise ValueError("batched launches compute T0-T5")
         self.ctab, self.stab, self.wtab = make_tables(n, angles)
         self.F = NF if full else 1
-        self.cfg = launch_config(n, self.a_count)
+        self.cfg = launch_config(n, self.a_count, batch=batch)
         self._res = None
 
     def out_shape(self):
-        return (self.a_count, self.F, self.n)
+        lead = (self.batch,) if self.batch > 1 else ()
+        return lead + (self.a_count, self.F, self.n)
+
+    def _med_elems(self):
+        return self.batch * self.a_count * 2 * self.n
+
+    def _circ_elems(self):
+        return self.batch * self.a_count * NF * 3
 
     def __call__(self, img: np.ndarray):
         img = np.ascontiguousarray(img, np.float32)
         out = np.empty(self.out_shape(), np.float32)
-        if self.full:
+        if self.batch > 1:
+            med = np.empty(self.out_shape()[:-2] + (2, self.n), np.int32)
+            rep = cuda_launch(self.ctx, TRACE_T05_BATCH, self.cfg,
+                              [cu_in(img), np.int32(self.n), cu_in(self.ctab), cu_in(self.stab), cu_in(self.wtab),
+                               cu_out(out), cu_out(med), np.int32(self.a0), np.int32(self.batch)])
+        elif self.full:
             med = np.empty((self.a_count, 2, self.n), np.int32)
             rep = cuda_launch(self.ctx, TRACE_T05, self.cfg,
                               [cu_in(img), np.int32(self.n), cu_in(self.ctab), cu_in(self.stab), cu_in(self.wtab),
@@ -97,18 +113,20 @@ class TraceTransform:
     def _resident(self):
         if self._res is None:
             ctx = self.ctx
-            r = {"img": ctx.mem_alloc(self.n * self.n * 4), "ctab": ctx.mem_alloc(self.ctab.nbytes),
+            r = {"img": ctx.mem_alloc(self.batch * self.n * self.n * 4), "ctab": ctx.mem_alloc(self.ctab.nbytes),
                  "stab": ctx.mem_alloc(self.stab.nbytes), "wtab": ctx.mem_alloc(self.wtab.nbytes),
                  "out": ctx.mem_alloc(int(np.prod(self.out_shape())) * 4),
-                 "med": ctx.mem_alloc(self.a_count * 2 * self.n * 4),
-                 "circ": ctx.mem_alloc(self.a_count * NF * 3 * 4)}
+                 "med": ctx.mem_alloc(self._med_elems() * 4),
+                 "circ": ctx.mem_alloc(self._circ_elems() * 4)}
             ctx.memcpy_htod(r["ctab"], self.ctab)
             ctx.memcpy_htod(r["stab"], self.stab)
             ctx.memcpy_htod(r["wtab"], self.wtab)
-            kern = TRACE_T05 if self.full else RADON
+            kern = TRACE_T05_BATCH if self.batch > 1 else (TRACE_T05 if self.full else RADON)
             types = ([(True, "f32"), (False, "i32"), (True, "f32"), (True, "f32"), (True, "f32"), (True, "f32"),
                       (True, "i32"), (False, "i32")] if self.full else
                      [(True, "f32"), (False, "i32"), (True, "f32"), (True, "f32"), (True, "f32"), (False, "i32")])
+            if self.batch > 1:
+                types = types + [(False, "i32")]
             from .api import render_module
             mh = ctx.module_load(render_module(kern, types, kern.name + "$resident"))
             r["fn"] = ctx.get_function(mh, kern.name)
@@ -121,7 +139,10 @@ class TraceTransform:
     def launch_resident(self):
         """Launch on the resident buffers (image already uploaded)."""
         r = self._resident()
-        if self.full:
+        if self.batch > 1:
+            args = [r["img"], np.int32(self.n), r["ctab"], r["stab"], r["wtab"], r["out"], r["med"],
+                    np.int32(self.a0), np.int32(self.batch)]
+        elif self.full:
             args = [r["img"], np.int32(self.n), r["ctab"], r["stab"], r["wtab"], r["out"], r["med"],
                     np.int32(self.a0)]
         else:
@@ -130,7 +151,7 @@ class TraceTransform:
         if not res.ok():
             raise RuntimeError(f"trace launch trapped: {res.trap}")
         if self.features:
-            rows = self.a_count * NF
+            rows = self.batch * self.a_count * NF
             res = self.ctx.launch(r["circus"], GridConfig(((rows + 7) // 8, 1, 1), (256, 1, 1)),
                                   [r["out"], np.int32(self.n), np.int32(rows), r["circ"]])
             if not res.ok():
@@ -139,13 +160,14 @@ class TraceTransform:
     def run_resident(self, img_host, out_host, med_host=None, circ_host=None):
         """H2D image -> fused kernel (-> circus) -> D2H sinograms (+ medians, + features)."""
         r = self._resident()
-        self.ctx.memcpy_htod(r["img"], img_host, self.n * self.n * 4)
+        self.ctx.memcpy_htod(r["img"], img_host, self.batch * self.n * self.n * 4)
         self.launch_resident()
-        self.ctx.memcpy_dtoh(out_host, r["out"], int(np.prod(self.out_shape())) * 4)
+        if out_host is not None:
+            self.ctx.memcpy_dtoh(out_host, r["out"], int(np.prod(self.out_shape())) * 4)
         if med_host is not None and self.full:
-            self.ctx.memcpy_dtoh(med_host, r["med"], self.a_count * 2 * self.n * 4)
+            self.ctx.memcpy_dtoh(med_host, r["med"], self._med_elems() * 4)
         if circ_host is not None and self.features:
-            self.ctx.memcpy_dtoh(circ_host, r["circ"], self.a_count * NF * 3 * 4)
+            self.ctx.memcpy_dtoh(circ_host, r["circ"], self._circ_elems() * 4)
 
     def resident_ptr(self, name: str) -> int:
         return self.ctx.device_pointer(self._resident()[name])
@@ -159,10 +181,10 @@ class TraceTransform:
 
 def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, stab_ptr: int, wtab_ptr: int,
                  out_ptr: int, med_ptr: int = 0, full: bool = True, sampler: int = 0, stream: int = 0,
-                 tex=None, pair_stride: int = 0) -> None:
-    """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex); pair_stride as in tt_b200.h."""
+                 tex=None, pair_stride: int = 0, batch: int = 1, img_stride: int = 0) -> None:
+    """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex); pair_stride, batch as in tt_b200.h."""
     d = _lib.TraceDesc(img_ptr, n, a0, a_count, int(full), ctab_ptr, stab_ptr, wtab_ptr or None, out_ptr,
-                       med_ptr or None, sampler, pair_stride)
+                       med_ptr or None, sampler, pair_stride, batch, 0, img_stride)
     if tex is not None:
         _check(lib.tt_trace_device_tex(C.byref(d), tex, C.c_void_p(stream)))
     else:
@@ -191,6 +213,18 @@ def image_texture(img_ptr: int, n: int, stream: int = 0):
     t = C.c_void_p()
     _check(lib.tt_image_tex_create(C.c_void_p(img_ptr), n, C.c_void_p(stream), C.byref(t)))
     return t
+
+
+def image_atlas(imgs_ptr: int, n: int, batch: int, img_stride: int = 0, stream: int = 0):
+    """Texture atlas of a device batch of images (tt_image_atlas_create)."""
+    t = C.c_void_p()
+    _check(lib.tt_image_atlas_create(C.c_void_p(imgs_ptr), n, batch, img_stride, C.c_void_p(stream), C.byref(t)))
+    return t
+
+
+def image_texture_update(t, imgs_ptr: int, img_stride: int = 0, stream: int = 0) -> None:
+    """Refresh a texture/atlas from device images (stream-ordered copy)."""
+    _check(lib.tt_image_tex_update(t, C.c_void_p(imgs_ptr), img_stride, C.c_void_p(stream)))
 
 
 def image_texture_destroy(t) -> None:
