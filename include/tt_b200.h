@@ -201,8 +201,10 @@ tt_status tt_events(tt_ctx* ctx, uint8_t* buf, size_t cap, size_t* needed);
 tt_status tt_make_tables(int n, int a_total, float* ctab, float* stab, float* wtab);
 /* Deterministic synthetic images: kind 0 disk-noise, 1 phantom, 2 sparse. */
 tt_status tt_synth_image(int kind, uint64_t seed, int n, float* img);
-/* Warps per line of the fused kernel for side n (the replay schedule). */
-int tt_schedule_warps(int n);
+/* Slots (lanes) per line of the fused kernel for side n: 8, 16 or 32 (one
+ * warp segment) or 32W (W warps) -- the reduction schedule the replay oracle
+ * mirrors. */
+int tt_schedule_slots(int n);
 /* Largest n the fused T0..T5 kernel supports. */
 int tt_max_full_n(void);
 

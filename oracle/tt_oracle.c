@@ -141,12 +141,21 @@ void tto_line_samples(const float* img, int n, float c, float s, int p, float* v
     }
 }
 
-/* Mirrors tt::schedule_warps (paper_1604_03410_b200/csrc/tt_kernels.cu):
- * the smallest power of two W with ceil(n / 32W) <= 32, clamped to [1, 16]. */
-int tto_schedule_warps(int n) {
+/* Mirrors tt::schedule_slots (paper_1604_03410_b200/csrc/tt_kernels.cu): the
+ * slots per line NS.  n <= 1024: one segment of 8, 16 or 32 lanes (the
+ * smallest with ceil(n/NS) <= 32; sub-warp segments need 32/NS | n, else 32);
+ * larger n: 32W lanes, W the smallest power of two with ceil(n/32W) <= 32,
+ * at most 16. */
+int tto_schedule_slots(int n) {
+    if (n <= 1024) {
+        int seg = 8;
+        while (seg < 32 && (n + seg - 1) / seg > 32) seg *= 2;
+        if (seg < 32 && n % (32 / seg) != 0) seg = 32;
+        return seg;
+    }
     int w = 1;
     while (w * 1024 < n && w < 16) w *= 2;
-    return w;
+    return 32 * w;
 }
 
 /* ----------------------------------------------------- f64 truth (§2.5) */
@@ -247,56 +256,65 @@ static void line_seq32(const float* v, float* sv, int n, const float* wtab, floa
 
 /* Warp butterfly: x_l <- x_l + x_{l^off}, off = 16..1 (commutative, so every
  * lane ends with the same value). */
-static float warp_butterfly(float x[32]) {
-    for (int off = 16; off >= 1; off >>= 1) {
+/* The kernel's reduction schedule is parameterised by NS, the slots (lanes)
+ * per line: LG = min(NS, 32) lanes form one warp or sub-warp segment, and
+ * NS / LG such groups (warps) share a line.  n <= 1024 uses one segment of 8,
+ * 16 or 32 lanes; larger n uses NS = 32W. */
+
+/* Butterfly over LG lanes: x_l <- x_l + x_{l^off}, off = LG/2..1 (commutative,
+ * so every lane ends with the same value). */
+static float warp_butterfly(float* x, int LG) {
+    for (int off = LG / 2; off >= 1; off >>= 1) {
         float y[32];
-        for (int l = 0; l < 32; ++l) y[l] = x[l] + x[l ^ off];
-        memcpy(x, y, sizeof(y));
+        for (int l = 0; l < LG; ++l) y[l] = x[l] + x[l ^ off];
+        memcpy(x, y, sizeof(float) * (size_t)LG);
     }
     return x[0];
 }
 
-/* Kogge-Stone inclusive scan: x_l <- x_{l-d} + x_l for l >= d. */
-static void warp_scan(float x[32]) {
-    for (int d = 1; d < 32; d <<= 1) {
+/* Kogge-Stone inclusive scan over LG lanes: x_l <- x_{l-d} + x_l for l >= d. */
+static void warp_scan(float* x, int LG) {
+    for (int d = 1; d < LG; d <<= 1) {
         float y[32];
-        for (int l = 0; l < 32; ++l) y[l] = (l >= d) ? x[l - d] + x[l] : x[l];
-        memcpy(x, y, sizeof(y));
+        for (int l = 0; l < LG; ++l) y[l] = (l >= d) ? x[l - d] + x[l] : x[l];
+        memcpy(x, y, sizeof(float) * (size_t)LG);
     }
 }
 
-/* Slot-strided sum over [0,len) with stride 32W, butterfly per warp,
- * sequential over warps (kernel pass 1 / pass 2 reduction order). */
-static float replay_strided_sum(const float* v, int len, int W) {
-    const int nslot = 32 * W;
+static int lanes_of(int NS) { return NS < 32 ? NS : 32; }
+
+/* Slot-strided sum over [0,len) with stride NS, butterfly per group,
+ * sequential over groups (kernel pass 1 / pass 2 reduction order). */
+static float replay_strided_sum(const float* v, int len, int NS) {
+    const int LG = lanes_of(NS);
     float total = 0.0f;
-    for (int w = 0; w < W; ++w) {
+    for (int w = 0; w < NS / LG; ++w) {
         float x[32];
-        for (int l = 0; l < 32; ++l) {
+        for (int l = 0; l < LG; ++l) {
             float acc = 0.0f;
-            for (int t = 32 * w + l; t < len; t += nslot) acc = acc + v[t];
+            for (int t = LG * w + l; t < len; t += NS) acc = acc + v[t];
             x[l] = acc;
         }
-        total = total + warp_butterfly(x);
+        total = total + warp_butterfly(x, LG);
     }
     return total;
 }
 
-/* Cooperative rescan of the crossing chunk (kernel: one warp, 32 elements
- * per block, Kogge-Stone scan per block, ballot for the first crossing). */
-static int replay_rescan(const float* u, int n, int start, int K, float exc, float S) {
+/* Cooperative rescan of the crossing chunk (kernel: one group of LG lanes,
+ * LG elements per block, Kogge-Stone scan per block, ballot). */
+static int replay_rescan(const float* u, int n, int start, int K, float exc, float S, int LG) {
     int len = n - start;
     if (len > K) len = K;
     float C = 0.0f;
-    for (int b = 0; b * 32 < len; ++b) {
+    for (int b = 0; b * LG < len; ++b) {
         float x[32];
-        for (int j = 0; j < 32; ++j) x[j] = (b * 32 + j < len) ? u[start + b * 32 + j] : 0.0f;
-        warp_scan(x);
-        for (int j = 0; j < 32 && b * 32 + j < len; ++j) {
+        for (int j = 0; j < LG; ++j) x[j] = (b * LG + j < len) ? u[start + b * LG + j] : 0.0f;
+        warp_scan(x, LG);
+        for (int j = 0; j < LG && b * LG + j < len; ++j) {
             float P = exc + (C + x[j]);
-            if (P + P >= S) return start + b * 32 + j;
+            if (P + P >= S) return start + b * LG + j;
         }
-        C = C + x[31];
+        C = C + x[LG - 1];
     }
     return len > 0 ? start + len - 1 : n - 1;
 }
@@ -321,42 +339,42 @@ static float chunk_sum(const float* u, int n, int start, int K) {
 }
 
 /* Weighted median of u under the kernel's schedule. */
-static int replay_median(const float* u, int n, float S, int W) {
-    const int nslot = 32 * W;
-    const int K = (n + nslot - 1) / nslot;
+static int replay_median(const float* u, int n, float S, int NS) {
+    const int LG = lanes_of(NS);
+    const int K = (n + NS - 1) / NS;
     float E = 0.0f;
-    for (int w = 0; w < W; ++w) {
+    for (int w = 0; w < NS / LG; ++w) {
         float c[32], inc[32];
-        for (int l = 0; l < 32; ++l) {
-            c[l] = chunk_sum(u, n, (32 * w + l) * K, K);
+        for (int l = 0; l < LG; ++l) {
+            c[l] = chunk_sum(u, n, (LG * w + l) * K, K);
             inc[l] = c[l];
         }
-        warp_scan(inc);
-        for (int l = 0; l < 32; ++l) {
+        warp_scan(inc, LG);
+        for (int l = 0; l < LG; ++l) {
             float e = (l == 0) ? 0.0f : inc[l - 1];
             float exc = E + e;
             float pend = exc + c[l];
-            if (pend + pend >= S) return replay_rescan(u, n, (32 * w + l) * K, K, exc, S);
+            if (pend + pend >= S) return replay_rescan(u, n, (LG * w + l) * K, K, exc, S, LG);
         }
-        E = E + inc[31];
+        E = E + inc[LG - 1];
     }
     return 0;
 }
 
 /* Medians + pass 2 for one line direction u (su = sqrt u) with the line's
  * S, S' (shared by both directions of a mirrored pair). */
-static void replay_emit(const float* u, const float* su, int n, const float* wtab, int W, float S, float Sp,
+static void replay_emit(const float* u, const float* su, int n, const float* wtab, int NS, float S, float Sp,
                         float out[6], int32_t med[2]) {
-    int m = replay_median(u, n, S, W);
-    int mp = replay_median(su, n, Sp, W);
+    const int LG = lanes_of(NS);
+    int m = replay_median(u, n, S, NS);
+    int mp = replay_median(su, n, Sp, NS);
     const int R = n - m, Rp = n - mp, Rmax = R > Rp ? R : Rp;
-    const int nslot = 32 * W;
     float tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int w = 0; w < W; ++w) {
+    for (int w = 0; w < NS / LG; ++w) {
         float x[8][32];
-        for (int l = 0; l < 32; ++l) {
+        for (int l = 0; l < LG; ++l) {
             float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int r = 32 * w + l; r < Rmax; r += nslot) {
+            for (int r = LG * w + l; r < Rmax; r += NS) {
                 float rf = (float)r, r2 = rf * rf;
                 float vv = (r < R) ? u[m + r] : 0.0f;
                 float ss = (r < Rp) ? su[mp + r] : 0.0f;
@@ -371,7 +389,7 @@ static void replay_emit(const float* u, const float* su, int n, const float* wta
             }
             for (int j = 0; j < 8; ++j) x[j][l] = a[j];
         }
-        for (int j = 0; j < 8; ++j) tot[j] = tot[j] + warp_butterfly(x[j]);
+        for (int j = 0; j < 8; ++j) tot[j] = tot[j] + warp_butterfly(x[j], LG);
     }
     out[0] = S;
     out[1] = tot[0];
@@ -400,7 +418,7 @@ static void put(float* out, int32_t* med, int F, int n, int row, int col, const 
  * partner angle a0+i+pair_stride (the mirrored line n-1-p of the same
  * samples when the tables are exactly mirrored, else sampled separately). */
 static void replay_unit(const float* img, int n, int a0, int units, int pair_stride, const float* ctab,
-                        const float* stab, const float* wtab, int full, int W, int i, int p, float* v, float* sv,
+                        const float* stab, const float* wtab, int full, int NS, int i, int p, float* v, float* sv,
                         float* rv, float* rsv, float* out, int32_t* med) {
     const int F = full ? TTO_NF : 1;
     const int nlines = (pair_stride > 0) ? 2 : 1;
@@ -410,11 +428,11 @@ static void replay_unit(const float* img, int n, int a0, int units, int pair_str
         if (n >= 2) tto_line_samples(img, n, ctab[a], stab[a], p, v);
         else for (int t = 0; t < n; ++t) v[t] = 0.0f;
         for (int t = 0; t < n; ++t) sv[t] = sqrtf(v[t]);
-        const float S = replay_strided_sum(v, n, W);
-        const float Sp = replay_strided_sum(sv, n, W);
+        const float S = replay_strided_sum(v, n, NS);
+        const float Sp = replay_strided_sum(sv, n, NS);
         float o[6] = {S, 0, 0, 0, 0, 0};
         int32_t md[2] = {0, 0};
-        if (full) replay_emit(v, sv, n, wtab, W, S, Sp, o, md);
+        if (full) replay_emit(v, sv, n, wtab, NS, S, Sp, o, md);
         put(out, med, F, n, i + li * units, p, o, md);
         if (mir) {
             for (int t = 0; t < n; ++t) {
@@ -423,16 +441,16 @@ static void replay_unit(const float* img, int n, int a0, int units, int pair_str
             }
             float o2[6] = {S, 0, 0, 0, 0, 0};
             int32_t md2[2] = {0, 0};
-            if (full) replay_emit(rv, rsv, n, wtab, W, S, Sp, o2, md2);
+            if (full) replay_emit(rv, rsv, n, wtab, NS, S, Sp, o2, md2);
             put(out, med, F, n, i + units, n - 1 - p, o2, md2);
         }
     }
 }
 
 void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stride, const float* ctab,
-                       const float* stab, const float* wtab, int full, int W, float* out, int32_t* med,
+                       const float* stab, const float* wtab, int full, int NS, float* out, int32_t* med,
                        int nthreads) {
-    if (W <= 0) W = tto_schedule_warps(n);
+    if (NS <= 0) NS = tto_schedule_slots(n);
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #else
@@ -444,7 +462,7 @@ void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stri
         float* buf = (float*)malloc(sizeof(float) * 4 * (size_t)(n > 0 ? n : 1));
 #pragma omp for schedule(dynamic, 64)
         for (long L = 0; L < total; ++L)
-            replay_unit(img, n, a0, units, pair_stride, ctab, stab, wtab, full, W, (int)(L / n), (int)(L % n), buf,
+            replay_unit(img, n, a0, units, pair_stride, ctab, stab, wtab, full, NS, (int)(L / n), (int)(L % n), buf,
                         buf + n, buf + 2 * (size_t)n, buf + 3 * (size_t)n, out, med);
         free(buf);
     }
@@ -469,7 +487,7 @@ void tto_transform(const float* img, int n, int a0, int a_count, int a_total, co
                    double* out64, double* absm, int nthreads) {
     (void)a_total;
     const int F = full ? TTO_NF : 1;
-    if (W <= 0) W = tto_schedule_warps(n);
+    if (W <= 0) W = tto_schedule_slots(n);
     if (mode == TTO_REPLAY) {
         int units, stride;
         tto_launch_structure(a_count, &units, &stride);
@@ -544,9 +562,9 @@ void tto_circus(const float* sino, int n, int rows, float* circ, double* circ64,
         for (int row = 0; row < rows; ++row) {
             const float* s = sino + (size_t)row * n;
             for (int p = 0; p + 1 < n; ++p) d[p] = fabsf(s[p + 1] - s[p]);
-            const float S = replay_strided_sum(s, n, 1);
-            const float P1 = replay_strided_sum(d, n - 1 > 0 ? n - 1 : 0, 1);
-            const int m = replay_median(s, n, S, 1);
+            const float S = replay_strided_sum(s, n, 32);
+            const float P1 = replay_strided_sum(d, n - 1 > 0 ? n - 1 : 0, 32);
+            const int m = replay_median(s, n, S, 32);
             float mx = 0.0f;
             for (int p = 0; p < n; ++p) mx = fmaxf(mx, s[p]);
             if (circ) {
@@ -600,11 +618,11 @@ long tto_check(const float* img, int n, int a0, int a_count, int a_total, const 
                double chain, double* stats, int nthreads) {
     (void)a_total;
     const int F = full ? TTO_NF : 1;
-    if (W <= 0) W = tto_schedule_warps(n);
-    const int K = (n + 32 * W - 1) / (32 * W);
-    /* fp32 chain length of the GPU schedule: slot partial + butterfly + warps
+    const int NS = W > 0 ? W : tto_schedule_slots(n);
+    const int K = (n + NS - 1) / NS;
+    /* fp32 chain length of the GPU schedule: slot partial + butterfly + groups
      * (callers checking a sequential fp32 result pass chain = n) */
-    if (chain <= 0.0) chain = (double)K + 5.0 + (double)W + 4.0;
+    if (chain <= 0.0) chain = (double)K + 5.0 + (double)(NS / 32 + 1) + 4.0;
     const double u = 1.0 / 16777216.0;
     const double atol_c = 2.0 * chain * u;
     const double eps = 2.0 * chain * u; /* median tie window */

@@ -56,8 +56,9 @@ void tto_synth(int kind, uint64_t seed, int n, float* img);
 /* The fp32 sampler for one line (a given by its c, s): v[t], t in [0,n). */
 void tto_line_samples(const float* img, int n, float c, float s, int p, float* v);
 
-/* Warps per line the B200 kernel uses for side n (the replay schedule). */
-int tto_schedule_warps(int n);
+/* Slots (lanes) per line the B200 kernel uses for side n: the replay schedule
+ * (8/16/32: one warp segment; 32W: W warps). */
+int tto_schedule_slots(int n);
 
 /*
  * Whole transform over angles [a0, a0+a_count) of a_total.
@@ -65,7 +66,7 @@ int tto_schedule_warps(int n);
  *   full=0: out[a][1][n] (T0 only)
  *   mode TTO_F64 also fills out64 (same layout, double) and absm (the
  *   condition numbers M_f of spec §2.5) when non-NULL.
- *   W is the replay schedule (TTO_REPLAY only; <=0 -> tto_schedule_warps).
+ *   W is the replay schedule NS = slots per line (TTO_REPLAY only; <=0 -> tto_schedule_slots).
  *   nthreads <= 0 -> OpenMP default.
  */
 void tto_transform(const float* img, int n, int a0, int a_count, int a_total,
@@ -78,7 +79,7 @@ void tto_transform(const float* img, int n, int a0, int a_count, int a_total,
  * units+i), processed as the mirrored line n-1-p of the same samples when
  * ctab/stab are exactly mirrored, else sampled separately. */
 void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stride, const float* ctab,
-                       const float* stab, const float* wtab, int full, int W, float* out, int32_t* med,
+                       const float* stab, const float* wtab, int full, int NS, float* out, int32_t* med,
                        int nthreads);
 
 /* Launch structure the native trace_t05/radon launcher uses for a_count

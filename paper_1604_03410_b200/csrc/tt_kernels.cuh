@@ -40,9 +40,10 @@ struct TraceArgs {
     int atlas_cols = 1;           // texture atlas tiles per row -- Texture sampler
 };
 
-// Warps per line of the fused kernel for side n — part of the reduction
-// schedule that oracle/tt_oracle.c TTO_REPLAY mirrors.
-int schedule_warps(int n);
+// Slots (lanes) per line of the fused kernel for side n: 8/16/32 (one warp
+// segment) or 32W (W warps) -- the reduction schedule that oracle/tt_oracle.c
+// TTO_REPLAY mirrors.
+int schedule_slots(int n);
 
 // Launch units for a drop-in launch of a_count angles: pairs (i, i+a_count/2)
 // when a_count is even (the kernel pairs mirrored angles).

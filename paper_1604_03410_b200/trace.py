@@ -42,8 +42,9 @@ def synth_image(kind: int, n: int, seed: int | None = None) -> np.ndarray:
     return img
 
 
-def schedule_warps(n: int) -> int:
-    return lib.tt_schedule_warps(n)
+def schedule_slots(n: int) -> int:
+    """Slots (lanes) per line of the fused kernel: 8/16/32 (warp segment) or 32W."""
+    return lib.tt_schedule_slots(n)
 
 
 def max_full_n() -> int:

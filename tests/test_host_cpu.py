@@ -52,8 +52,8 @@ def test_synthetic_images_bit_identical_to_oracle(kind, n):
 
 
 def test_schedule_matches_oracle_replay_schedule():
-    for n in (1, 16, 300, 512, 1024, 1500, 2048, 4095, 4096, 8192, 16384):
-        assert tt.schedule_warps(n) == O.schedule_warps(n)
+    for n in (1, 2, 16, 64, 100, 101, 255, 256, 300, 512, 777, 1000, 1024, 1500, 2048, 4095, 4096, 8192, 16384):
+        assert tt.schedule_slots(n) == O.schedule_slots(n)
 
 
 def test_no_gpu_fails_loudly():
