@@ -219,12 +219,15 @@ def run_ours(args, ws, rank, local):
         med = torch.empty((B, a_cnt, 2, n), dtype=torch.int32, device="cuda")
         circ = torch.empty((B, a_cnt, F, 3), device="cuda")
         flush = torch.empty(int(256 << 20) // 4, device="cuda")  # > 126 MB L2
+        wsoa = torch.empty(6 * n, device="cuda") if full else None  # pass-2 weight layout (constant of n)
         gathered = torch.empty((A, F, n), device="cuda") if orient else None
         gathered_raw = torch.empty((ws * a_cnt, F, n), device="cuda") if orient else None
         feats = torch.empty((ws * B, a_cnt, F, 3), device="cuda") if (ws > 1 and not orient) else None
     tex = None
     if args.sampler == 1:  # texture layout of this step's image(s); refreshed inside every timed step
         tex = image_atlas(img.data_ptr(), n, B, 0, sptr) if B > 1 else image_texture(img.data_ptr(), n, sptr)
+    if full:
+        tt.weights_soa(wtab.data_ptr(), n, wsoa.data_ptr(), sptr)
     launches_per_step = 1 + (1 if feats_on else 0) + (1 if tex is not None and B > 1 else 0)
 
     def step():
@@ -232,7 +235,7 @@ def run_ours(args, ws, rank, local):
             image_texture_update(tex, img.data_ptr(), 0, sptr)
         tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
                         out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
-                        pair_stride=pair, batch=B)
+                        pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0)
 
     def features():
         if feats_on:  # P-functional (circus) stage consuming the sinograms

@@ -244,8 +244,16 @@ typedef struct tt_trace_desc {
                            at out + b*rows*F*n and med + b*rows*2*n (rows = a_count) */
     int32_t _pad2;
     int64_t img_stride; /* elements between images (0: n*n) */
+    const float* wsoa;  /* optional pass-2 weight layout of wtab (tt_weights_soa, 24n bytes,
+                           16-B aligned); NULL: converted into stream-ordered scratch per call */
 } tt_trace_desc;
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
+
+/* Regroup a [n][8] weight table (tt_make_tables) on device into the fused
+ * kernel's pass-2 layout: [n] x (w3re, w3im, w4re, w4im) then [n] x (w5re,
+ * w5im) -- 24n bytes at d_wsoa.  Pass the result as tt_trace_desc.wsoa to
+ * reuse it across launches. */
+tt_status tt_weights_soa(const float* d_wtab, int n, float* d_wsoa, void* stream);
 
 /* P-functionals (circus features) of `rows` sinogram rows of
  * length n on device: circ[row][3] = (total variation, value at the weighted

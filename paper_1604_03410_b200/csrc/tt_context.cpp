@@ -119,6 +119,14 @@ struct TexEntry {
     cudaTextureObject_t tex = 0;
 };
 
+// Pass-2 weight layout (tt::launch_weights_soa) cached per wtab allocation,
+// rebuilt only when the allocation's generation changed.
+struct WeightEntry {
+    std::uint64_t gen = ~0ull;
+    int n = 0;
+    float* d = nullptr;
+};
+
 struct LaunchRecord {
     std::string kernel;
     std::uint32_t grid[3] = {1, 1, 1};
@@ -163,10 +171,18 @@ struct tt_ctx {
     std::uint64_t h2d_mark = 0, d2h_mark = 0;
 
     std::string last_error;
-    std::map<std::uint64_t, TexEntry> tex_cache;  // keyed by image allocation base
+    std::map<std::uint64_t, TexEntry> tex_cache;      // keyed by image allocation base
+    std::map<std::uint64_t, WeightEntry> w_cache;     // keyed by wtab allocation base
 };
 
 namespace {
+
+void drop_weights(tt_ctx* ctx, std::uint64_t base) {
+    auto it = ctx->w_cache.find(base);
+    if (it == ctx->w_cache.end()) return;
+    if (it->second.d) cudaFreeAsync(it->second.d, ctx->stream);  // stream-ordered after its readers
+    ctx->w_cache.erase(it);
+}
 
 void drop_texture(tt_ctx* ctx, std::uint64_t base) {
     auto it = ctx->tex_cache.find(base);
@@ -535,8 +551,29 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
         ta.atlas_cols = te.cols;
         ta.tex = te.tex;
     }
+    int extra_launches = 0;
+    if (full) {
+        WeightEntry& we = ctx.w_cache[wt->base];
+        if (we.d == nullptr || we.n != n || we.gen != wt->gen) {
+            if (we.d == nullptr || we.n != n) {
+                if (we.d) cudaFreeAsync(we.d, ctx.stream);
+                we = WeightEntry{};
+                cudaError_t e = cudaMallocAsync((void**)&we.d, tt::weights_soa_bytes(n), ctx.stream);
+                if (e != cudaSuccess) {
+                    ctx.w_cache.erase(wt->base);
+                    return cuda_outcome(e, "weight table");
+                }
+                we.n = n;
+            }
+            cudaError_t e = tt::launch_weights_soa(ta.wtab, n, we.d, ctx.stream);
+            if (e != cudaSuccess) return cuda_outcome(e, "weight table");
+            we.gen = wt->gen;
+            extra_launches = 1;
+        }
+        ta.wsoa = we.d;
+    }
     o = cuda_outcome(tt::launch_trace(ta, ctx.stream), "trace kernel");
-    o.gpu_launches = tt::trace_launch_count(ta);
+    o.gpu_launches = tt::trace_launch_count(ta) + extra_launches;
     return o;
 }
 
@@ -706,6 +743,7 @@ tt_status tt_ctx_destroy(tt_ctx* ctx) {
     DeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     while (!ctx->tex_cache.empty()) drop_texture(ctx, ctx->tex_cache.begin()->first);
+    while (!ctx->w_cache.empty()) drop_weights(ctx, ctx->w_cache.begin()->first);
     for (auto& kv : ctx->allocs)
         if (kv.second.live && kv.second.dptr) cudaFreeAsync(kv.second.dptr, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
@@ -838,6 +876,7 @@ tt_status tt_mem_free(tt_ctx* ctx, tt_devptr p) {
         return fail(ctx, TT_ERR_DOUBLE_FREE, "DoubleFree: device pointer already freed");
     DeviceGuard guard(ctx->device);
     drop_texture(ctx, p.base);
+    drop_weights(ctx, p.base);
     cudaError_t e = cudaFreeAsync(it->second.dptr, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFreeAsync");
     it->second.live = false;  // the address stays reserved: never reused
@@ -1069,8 +1108,8 @@ static tt_status check_desc(const tt_trace_desc* d) {
         return fail(nullptr, TT_ERR_INVALID, "img_stride smaller than one image");
     if (!d->ctab || !d->stab || !d->out || (d->full && !d->wtab))
         return fail(nullptr, TT_ERR_INVALID, "null table or output pointer");
-    if (d->full && (reinterpret_cast<std::uintptr_t>(d->wtab) & 15u))
-        return fail(nullptr, TT_ERR_INVALID, "wtab must be 16-byte aligned");
+    if (d->full && ((reinterpret_cast<std::uintptr_t>(d->wtab) | reinterpret_cast<std::uintptr_t>(d->wsoa)) & 15u))
+        return fail(nullptr, TT_ERR_INVALID, "wtab / wsoa must be 16-byte aligned");
     return TT_OK;
 }
 
@@ -1091,6 +1130,7 @@ static tt::TraceArgs to_args(const tt_trace_desc* d) {
     ta.ctab = d->ctab;
     ta.stab = d->stab;
     ta.wtab = d->wtab;
+    ta.wsoa = d->wsoa;
     ta.out = d->out;
     ta.med = d->med;
     ta.full = d->full != 0;
@@ -1099,12 +1139,40 @@ static tt::TraceArgs to_args(const tt_trace_desc* d) {
     return ta;
 }
 
+// Raw-pointer launches without a prepared weight layout convert wtab into
+// stream-ordered scratch around the launch (one extra small kernel).
+struct WeightScratch {
+    float* d = nullptr;
+    cudaStream_t s = nullptr;
+    ~WeightScratch() {
+        if (d) cudaFreeAsync(d, s);
+    }
+    cudaError_t prepare(tt::TraceArgs& ta, cudaStream_t stream) {
+        if (!ta.full || ta.wsoa) return cudaSuccess;
+        s = stream;
+        cudaError_t e = cudaMallocAsync((void**)&d, tt::weights_soa_bytes(ta.n), stream);
+        if (e != cudaSuccess) return e;
+        ta.wsoa = d;
+        return tt::launch_weights_soa(ta.wtab, ta.n, d, stream);
+    }
+};
+
+tt_status tt_weights_soa(const float* d_wtab, int n, float* d_wsoa, void* stream) {
+    if (!d_wtab || !d_wsoa || n < 1) return fail(nullptr, TT_ERR_INVALID, "bad weight-table arguments");
+    if ((reinterpret_cast<std::uintptr_t>(d_wtab) | reinterpret_cast<std::uintptr_t>(d_wsoa)) & 15u)
+        return fail(nullptr, TT_ERR_INVALID, "weight tables must be 16-byte aligned");
+    cudaError_t e = tt::launch_weights_soa(d_wtab, n, d_wsoa, (cudaStream_t)stream);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "weight table");
+}
+
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream) {
     tt_status st = check_desc(d);
     if (st != TT_OK) return st;
     if (!d->img) return fail(nullptr, TT_ERR_INVALID, "null image");
     tt::TraceArgs ta = to_args(d);
     cudaStream_t s = (cudaStream_t)stream;
+    WeightScratch ws;
+    if (cudaError_t e = ws.prepare(ta, s); e != cudaSuccess) return cuda_fail(nullptr, e, "weight table");
     if (d->sampler == 1) {
         cudaArray_t arr = nullptr;
         ta.sampler = tt::Sampler::Texture;
@@ -1200,6 +1268,9 @@ tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, voi
     ta.sampler = tt::Sampler::Texture;
     ta.tex = t->tex;
     ta.atlas_cols = t->cols;
+    WeightScratch ws;
+    if (cudaError_t e = ws.prepare(ta, (cudaStream_t)stream); e != cudaSuccess)
+        return cuda_fail(nullptr, e, "weight table");
     cudaError_t e = tt::launch_trace(ta, (cudaStream_t)stream);
     return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "trace kernel");
 }

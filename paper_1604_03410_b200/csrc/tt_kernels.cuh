@@ -9,6 +9,7 @@
 // emulator.hpp:747-793); these kernels replace that engine.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -31,6 +32,7 @@ struct TraceArgs {
     const float* ctab = nullptr;  // [A_total] cos(theta_a), f64 -> f32 on host
     const float* stab = nullptr;  // [A_total] sin(theta_a)
     const float* wtab = nullptr;  // [n][8]: r, r^2, w3re, w3im, w4re, w4im, w5re, w5im (spec §2.2), 16-B aligned
+    const float* wsoa = nullptr;  // full: launch_weights_soa(wtab) -- [n] float4 (w3, w4) then [n] float2 (w5)
     float* out = nullptr;         // full: [rows][6][n]; T0-only: [rows][n]; rows = a_count*(1+paired)
     int32_t* med = nullptr;       // full: [rows][2][n] (m, m'), may be null
     bool full = true;             // T0..T5 (else T0 / Radon only)
@@ -56,6 +58,13 @@ inline void launch_structure(int a_count, int* units, int* pair_stride) {
         *pair_stride = 0;
     }
 }
+
+// Pass-2 weight layout: the complex weights of wtab regrouped as [n] float4
+// (w3re, w3im, w4re, w4im) followed by [n] float2 (w5re, w5im), so a warp's
+// weight loads for 32 consecutive r are two fully used contiguous spans
+// (r and r^2 are formed in registers, bit-identical to wtab's first columns).
+inline std::size_t weights_soa_bytes(int n) { return std::size_t(n) * 24; }
+cudaError_t launch_weights_soa(const float* wtab, int n, float* wsoa, cudaStream_t s);
 
 // Largest n the fused T0-T5 kernel supports (line buffer must fit in smem).
 int max_full_n();

@@ -182,14 +182,20 @@ class TraceTransform:
 
 def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, stab_ptr: int, wtab_ptr: int,
                  out_ptr: int, med_ptr: int = 0, full: bool = True, sampler: int = 0, stream: int = 0,
-                 tex=None, pair_stride: int = 0, batch: int = 1, img_stride: int = 0) -> None:
-    """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex); pair_stride, batch as in tt_b200.h."""
+                 tex=None, pair_stride: int = 0, batch: int = 1, img_stride: int = 0, wsoa_ptr: int = 0) -> None:
+    """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex); pair_stride, batch, wsoa as in
+    tt_b200.h (wsoa_ptr: a prepared weights_soa() buffer; 0 converts wtab per call)."""
     d = _lib.TraceDesc(img_ptr, n, a0, a_count, int(full), ctab_ptr, stab_ptr, wtab_ptr or None, out_ptr,
-                       med_ptr or None, sampler, pair_stride, batch, 0, img_stride)
+                       med_ptr or None, sampler, pair_stride, batch, 0, img_stride, wsoa_ptr or None)
     if tex is not None:
         _check(lib.tt_trace_device_tex(C.byref(d), tex, C.c_void_p(stream)))
     else:
         _check(lib.tt_trace_device(C.byref(d), C.c_void_p(stream)))
+
+
+def weights_soa(wtab_ptr: int, n: int, wsoa_ptr: int, stream: int = 0) -> None:
+    """Regroup a device [n][8] weight table into the pass-2 layout (tt_weights_soa; 24n bytes)."""
+    _check(lib.tt_weights_soa(C.c_void_p(wtab_ptr), n, C.c_void_p(wsoa_ptr), C.c_void_p(stream)))
 
 
 def circus_device(sino_ptr: int, n: int, rows: int, circ_ptr: int, stream: int = 0) -> None:

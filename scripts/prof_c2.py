@@ -18,10 +18,13 @@ img = torch.from_numpy(tt.synth_image(tt.DISK, n)).cuda()
 ct, st, wt = (torch.from_numpy(x).cuda() for x in (c, s, w))
 out = torch.empty((A, 6 if full else 1, n), device="cuda")
 med = torch.empty((A, 2, n), dtype=torch.int32, device="cuda")
+wsoa = torch.empty(6 * n, device="cuda")
+tt.weights_soa(wt.data_ptr(), n, wsoa.data_ptr(), torch.cuda.current_stream().cuda_stream)
+torch.cuda.synchronize()
 stream = torch.cuda.current_stream().cuda_stream
 tex = image_texture(img.data_ptr(), n, stream) if sampler == 1 else None
 for _ in range(reps):
     tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
-                    med.data_ptr(), full=full, sampler=sampler, stream=stream, tex=tex)
+                    med.data_ptr(), full=full, sampler=sampler, stream=stream, tex=tex, wsoa_ptr=wsoa.data_ptr())
 torch.cuda.synchronize()
 print("ok", float(out[:, 0].sum()))

@@ -29,10 +29,13 @@ def run_point(n, A, full, stream, flush, reps, peak):
     med = torch.empty((A, 2, n), dtype=torch.int32, device="cuda") if full else None
     sp = stream.cuda_stream
     tex = image_texture(img.data_ptr(), n, sp)
+    wsoa = torch.empty(6 * n, device="cuda")
+    tt.weights_soa(wt.data_ptr(), n, wsoa.data_ptr(), sp)
 
     def launch():
         tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
-                        med.data_ptr() if full else 0, full=full, sampler=1, stream=sp, tex=tex)
+                        med.data_ptr() if full else 0, full=full, sampler=1, stream=sp, tex=tex,
+                        wsoa_ptr=wsoa.data_ptr())
 
     for _ in range(2):
         launch()

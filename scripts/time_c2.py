@@ -17,6 +17,9 @@ img = torch.from_numpy(tt.synth_image(tt.DISK, n)).cuda()
 ct, st, wt = (torch.from_numpy(x).cuda() for x in (c, s, w))
 out = torch.empty((A, 6, n), device="cuda")
 med = torch.empty((A, 2, n), dtype=torch.int32, device="cuda")
+wsoa = torch.empty(6 * n, device="cuda")
+tt.weights_soa(wt.data_ptr(), n, wsoa.data_ptr(), torch.cuda.current_stream().cuda_stream)
+torch.cuda.synchronize()
 flush = torch.empty(64 << 20, device="cuda")
 stream = torch.cuda.Stream()
 sp = stream.cuda_stream
@@ -28,7 +31,7 @@ for i in range(25):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
-                    med.data_ptr(), stream=sp, tex=tex)
+                    med.data_ptr(), stream=sp, tex=tex, wsoa_ptr=wsoa.data_ptr())
     e1.record(stream)
     e1.synchronize()
     if i >= 5:

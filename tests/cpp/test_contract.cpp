@@ -106,7 +106,7 @@ int main() {
                       rmed.data(), nullptr, nullptr, 0);
         CHECK(std::memcmp(out.data(), ref.data(), out.size() * 4) == 0);
         CHECK(med == rmed);
-        CHECK(ctx.counters().gpu_kernel_launches == 1);
+        CHECK(ctx.counters().gpu_kernel_launches == 2);  // pass-2 weight layout of the uploaded wtab + fused kernel
     }
     std::printf("%s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
     return failures ? 1 : 0;

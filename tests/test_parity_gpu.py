@@ -258,3 +258,29 @@ def test_tiny_and_denormal_values_exact(ctx):
         tr, out, med = _run(ctx, img, n, A, sampler=sampler)
         rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
         assert _bitwise_equal(out, rout) and np.array_equal(med, rmed)
+
+
+@pytest.mark.parametrize("n,A", [(256, 12), (1000, 6), (1024, 8)])
+def test_prepared_weight_layout_equals_per_call_conversion(ctx, n, A):
+    """tt_weights_soa + tt_trace_desc.wsoa gives the same bits as the per-call conversion."""
+    img = tt.synth_image(tt.PHANTOM, n)
+    c, s, w = tt.make_tables(n, A)
+    ref, rmed = _raw(ctx, img, n, c, s, w, 0, A, 0)
+    bufs = {k: ctx.mem_alloc(x.nbytes) for k, x in (("img", img), ("c", c), ("s", s), ("w", w))}
+    for k, x in (("img", img), ("c", c), ("s", s), ("w", w)):
+        ctx.memcpy_htod(bufs[k], np.ascontiguousarray(x))
+    ws = ctx.mem_alloc(24 * n)
+    out_d, med_d = ctx.mem_alloc(A * 6 * n * 4), ctx.mem_alloc(A * 2 * n * 4)
+    ptr = {k: ctx.device_pointer(v) for k, v in bufs.items()}
+    tt.weights_soa(ptr["w"], n, ctx.device_pointer(ws), ctx.stream)
+    for _ in range(2):  # reused across launches
+        tt.trace_device(ptr["img"], n, 0, A, ptr["c"], ptr["s"], ptr["w"], ctx.device_pointer(out_d),
+                        ctx.device_pointer(med_d), stream=ctx.stream, wsoa_ptr=ctx.device_pointer(ws))
+    ctx.synchronize()
+    out = np.empty((A, 6, n), np.float32)
+    med = np.empty((A, 2, n), np.int32)
+    ctx.memcpy_dtoh(out, out_d)
+    ctx.memcpy_dtoh(med, med_d)
+    for b in list(bufs.values()) + [ws, out_d, med_d]:
+        ctx.mem_free(b)
+    assert _bitwise_equal(out, ref) and np.array_equal(med, rmed)
