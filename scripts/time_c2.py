@@ -1,4 +1,4 @@
-"""Time the fused kernel on C2 (or TT_N/TT_A) with CUDA events; prints one JSON line.
+"""Time the fused kernel on C2 (or TT_N/TT_A; TT_FULL=0 for T0 only) with CUDA events; one JSON line.
 Use TT_LIB_PATH to time an experimental library variant."""
 import json
 import os
@@ -12,30 +12,32 @@ from paper_1604_03410_b200.trace import image_texture  # noqa: E402
 
 n = int(os.environ.get("TT_N", "1024"))
 A = int(os.environ.get("TT_A", "720"))
+full = os.environ.get("TT_FULL", "1") == "1"
+reps = int(os.environ.get("TT_REPS", "20"))
+F = 6 if full else 1
 c, s, w = tt.make_tables(n, A)
 img = torch.from_numpy(tt.synth_image(tt.DISK, n)).cuda()
 ct, st, wt = (torch.from_numpy(x).cuda() for x in (c, s, w))
-out = torch.empty((A, 6, n), device="cuda")
+out = torch.empty((A, F, n), device="cuda")
 med = torch.empty((A, 2, n), dtype=torch.int32, device="cuda")
 wsoa = torch.empty(6 * n, device="cuda")
-tt.weights_soa(wt.data_ptr(), n, wsoa.data_ptr(), torch.cuda.current_stream().cuda_stream)
-torch.cuda.synchronize()
 flush = torch.empty(64 << 20, device="cuda")
 stream = torch.cuda.Stream()
 sp = stream.cuda_stream
+tt.weights_soa(wt.data_ptr(), n, wsoa.data_ptr(), sp)
 tex = image_texture(img.data_ptr(), n, sp)
 ts = []
-for i in range(25):
+for i in range(reps + 3):
     with torch.cuda.stream(stream):
         flush.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
-                    med.data_ptr(), stream=sp, tex=tex, wsoa_ptr=wsoa.data_ptr())
+                    med.data_ptr() if full else 0, full=full, stream=sp, tex=tex, wsoa_ptr=wsoa.data_ptr())
     e1.record(stream)
     e1.synchronize()
-    if i >= 5:
+    if i >= 3:
         ts.append(e0.elapsed_time(e1))
 ts.sort()
-print(json.dumps({"lib": os.environ.get("TT_LIB_PATH", "default"), "n": n, "A": A, "median_ms": ts[len(ts) // 2],
-                  "min_ms": ts[0], "checksum": float(out.double().sum())}))
+print(json.dumps({"lib": os.environ.get("TT_LIB_PATH", "default"), "n": n, "A": A, "full": full,
+                  "median_ms": ts[len(ts) // 2], "min_ms": ts[0], "checksum": float(out.double().sum())}))
