@@ -15,7 +15,7 @@ image of the workload:
   c1: 256^2, 360 angles (the reference's CPU-runnable case).
 `value` times the fused kernel on device-resident inputs (CUDA events on the
 launching stream, L2 flushed between steps, max over ranks); `e2e` times the
-public API (TraceTransform.run_resident: pinned H2D of the image, the launch,
+public API (tt.Plan.run / tt_plan_run: pinned H2D of the image, the chunked launches,
 D2H of sinograms + medians).  `--impl reference` runs the reference's own
 execution engine (oracle/_ref: the gridjit emulator running
 oracle/trace_t05.krn) on a bounded sample, on all host cores.
@@ -299,8 +299,8 @@ def run_ours(args, ws, rank, local):
     ctx = tt.create_context(local)
     ctx.set_sampler(args.sampler)
     # public API on this rank's share (contiguous angle block under torchrun c3)
-    tr = tt.TraceTransform(ctx, n, A, full=full, a0=rank * a_cnt if orient else 0, a_count=a_cnt,
-                           features=feats_on, batch=B)
+    plan = tt.Plan(ctx, n, A, full=full, a0=rank * a_cnt if orient else 0, a_count=a_cnt, features=feats_on,
+                   batch=B)
     nb_img, nb_out = B * n * n * 4, B * a_cnt * F * n * 4
     nb_med, nb_circ = B * a_cnt * 2 * n * 4, B * a_cnt * F * 3 * 4
     # feature extraction (c4) returns the features; the sinogram workloads return sinograms + medians
@@ -315,13 +315,13 @@ def run_ours(args, ws, rank, local):
     h_circ = np.ctypeslib.as_array((C.c_float * (nb_circ // 4)).from_address(hp[3].value))
     img_arg = h_img if B > 1 else h_img[0]
     for _ in range(max(2, min(args.warmup, 3) if images else args.warmup)):
-        tr.run_resident(img_arg, h_out, h_med if full else None, h_circ if feats_on else None)
+        plan.run(img_arg, h_out, h_med if full else None, h_circ if feats_on else None)
     e2e_steps = max(3, min(args.steps, 5 if images else 50))
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        tr.run_resident(img_arg, h_out, h_med if full else None, h_circ if feats_on else None)
+        plan.run(img_arg, h_out, h_med if full else None, h_circ if feats_on else None)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if dist:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
@@ -330,15 +330,14 @@ def run_ours(args, ws, rank, local):
     d2h = (nb_out + (nb_med if full else 0) if want_sino else 0) + (nb_circ if feats_on else 0)
     e2e = {"value": samples_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nb_img, "d2h_bytes_per_step": d2h,
            "ms_per_step": e2e_s * 1e3,
-           "api": ("TraceTransform.run_resident -> tt_memcpy_htod / tt_launch(" +
-                   ("trace_t05_batch" if B > 1 else "trace_t05") + (", circus" if feats_on else "") +
-                   ") / tt_memcpy_dtoh")}
+           "api": f"tt.Plan.run -> tt_plan_run (pinned H2D, {plan.chunks} chunked fused-kernel launches with "
+                  "overlapped D2H of finished rows" + (", circus" if feats_on else "") + ")"}
     # parity spot check of the e2e output against the device-resident one
     if want_sino and not orient:
         same = np.array_equal(h_out.reshape(out.shape), out.cpu().numpy())
     else:
         same = np.array_equal(h_circ.reshape(circ.shape), circ.cpu().numpy())
-    tr.free_resident()
+    plan.destroy()
     ctx.destroy()
     for hh in hp:
         lib.tt_host_free(hh)

@@ -273,6 +273,35 @@ tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, int64_t img_
 tt_status tt_image_tex_destroy(tt_image_tex* t);
 tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, void* stream);
 
+/* ---- plans: the host-to-host form of the path -------------------------------
+ * One plan = one (n, angles, functionals, batch) configuration with its device
+ * tables, image texture and output buffers resident.  tt_plan_run uploads the
+ * image(s), runs the fused kernel in `chunks` angle chunks over two compute
+ * streams while a copy stream downloads each finished chunk's rows (overlapped
+ * D2H), runs the P-functional stage once over the sinogram, and returns when
+ * every requested host buffer is filled.  Results equal one whole launch
+ * bit-for-bit.  Host buffers should be pinned (tt_host_alloc) for the copies to
+ * overlap.  The caller-side flow this replaces is cuda_launch's
+ * marshal -> launch -> download sequence (autolaunch.hpp:167-245) repeated per
+ * image; counters (bytes_h2d / bytes_d2h / gpu_kernel_launches) are updated. */
+typedef struct tt_plan tt_plan;
+typedef struct tt_plan_desc {
+    int32_t n;        /* image side (= line length = lines per angle) */
+    int32_t a_total;  /* angle grid: theta_a = 2 pi a / a_total (tt_make_tables) */
+    int32_t a0;       /* first angle of this plan */
+    int32_t a_count;  /* angles a0 .. a0 + a_count - 1 */
+    int32_t full;     /* 1: T0..T5 (+ medians), 0: T0 (Radon) only */
+    int32_t features; /* 1: P-functionals (circus) after the trace (full only) */
+    int32_t batch;    /* images per run (0 or 1: one) */
+    int32_t chunks;   /* pipeline chunks (0: automatic; batched plans use 1) */
+} tt_plan_desc;
+tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out);
+/* h_img [batch][n][n]; h_out [batch][a_count][F][n], h_med [batch][a_count][2][n],
+ * h_circ [batch][a_count][6][3] -- each output may be NULL (not downloaded). */
+tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, int32_t* h_med, float* h_circ);
+tt_status tt_plan_chunks(const tt_plan* p, int* chunks);
+tt_status tt_plan_destroy(tt_plan* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,6 @@ from .api import (  # noqa: F401
     native_kernels, parse_kernel, render_module,
 )
 from .trace import (  # noqa: F401
-    CIRCUS, DISK, PHANTOM, SEEDS, SPARSE, TRACE_T05, TRACE_T05_BATCH, RADON, TraceTransform, circus, circus_device, make_tables,
+    CIRCUS, DISK, PHANTOM, SEEDS, SPARSE, Plan, TRACE_T05, TRACE_T05_BATCH, RADON, TraceTransform, circus, circus_device, make_tables,
     max_full_n, schedule_slots, synth_image, trace_device, weights_soa,
 )

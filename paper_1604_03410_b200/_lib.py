@@ -48,6 +48,10 @@ class Counters(C.Structure):
                                           "gpu_kernel_launches")]
 
 
+class PlanDesc(C.Structure):
+    _fields_ = [(k, C.c_int32) for k in ("n", "a_total", "a0", "a_count", "full", "features", "batch", "chunks")]
+
+
 class TraceDesc(C.Structure):
     _fields_ = [("img", C.c_void_p), ("n", C.c_int32), ("a0", C.c_int32), ("a_count", C.c_int32),
                 ("full", C.c_int32), ("ctab", C.c_void_p), ("stab", C.c_void_p), ("wtab", C.c_void_p),
@@ -101,6 +105,10 @@ _sigs = {
     "tt_image_tex_update": (_S, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "tt_image_tex_destroy": (_S, [C.c_void_p]),
     "tt_trace_device_tex": (_S, [C.POINTER(TraceDesc), C.c_void_p, C.c_void_p]),
+    "tt_plan_create": (_S, [C.c_void_p, C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]),
+    "tt_plan_run": (_S, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tt_plan_chunks": (_S, [C.c_void_p, C.POINTER(C.c_int)]),
+    "tt_plan_destroy": (_S, [C.c_void_p]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(lib, _name)

@@ -1276,3 +1276,245 @@ tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, voi
 }
 
 }  // extern "C"
+
+// ----------------------------------------------------------------- plans
+//
+// A plan is the host-to-host form of the path (include/tt_b200.h
+// tt_plan_*): the device tables, image texture and output buffers live for
+// the plan's lifetime, and tt_plan_run pipelines one call.  The fused
+// kernel is launched in angle chunks alternating over two compute streams
+// while a copy stream downloads each finished chunk's sinogram rows (and
+// median rows), so the device-to-host transfer overlaps the remaining
+// chunks; the P-functional stage runs once over the whole sinogram.  The
+// chunked launches write exactly the rows of one whole launch (a chunk is
+// the contiguous unit range [u0, u1) plus its mirror rows, partner_row =
+// U), so the outputs are bit-identical to the single-launch path.
+
+struct tt_plan {
+    tt_ctx* ctx = nullptr;
+    tt_plan_desc d{};
+    int F = 1, units = 0, pair = 0, chunks = 1;
+    float *img = nullptr, *ctab = nullptr, *stab = nullptr, *wtab = nullptr, *wsoa = nullptr;
+    float *out = nullptr, *circ = nullptr;
+    std::int32_t* med = nullptr;
+    cudaArray_t arr = nullptr;
+    cudaTextureObject_t tex = 0;
+    int cols = 1;
+    cudaStream_t sc[2] = {nullptr, nullptr}, sx = nullptr;
+    std::vector<cudaEvent_t> done;  // per chunk: its rows are final
+    cudaEvent_t ready = nullptr, traced = nullptr;
+};
+
+namespace {
+
+void plan_release(tt_plan* p) {
+    if (!p) return;
+    DeviceGuard guard(p->ctx->device);
+    for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx})
+        if (s) cudaStreamSynchronize(s);
+    for (cudaEvent_t e : p->done) cudaEventDestroy(e);
+    if (p->ready) cudaEventDestroy(p->ready);
+    if (p->traced) cudaEventDestroy(p->traced);
+    if (p->tex) cudaDestroyTextureObject(p->tex);
+    if (p->arr) cudaFreeArray(p->arr);
+    for (void* b : {(void*)p->img, (void*)p->ctab, (void*)p->stab, (void*)p->wtab, (void*)p->wsoa, (void*)p->out,
+                    (void*)p->circ, (void*)p->med})
+        if (b) cudaFree(b);
+    for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx})
+        if (s) cudaStreamDestroy(s);
+    delete p;
+}
+
+}  // namespace
+
+extern "C" {
+
+tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
+    if (!ctx || ctx->destroyed || !d || !out) return fail(ctx, TT_ERR_INVALID, "bad plan arguments");
+    *out = nullptr;
+    const int n = d->n;
+    if (n < 1 || n > (d->full ? tt::max_full_n() : 32768))
+        return fail(ctx, TT_ERR_LAUNCH_CONFIG, "LaunchConfigError: n out of range for the native kernel");
+    if (d->a_total < 1 || d->a0 < 0 || d->a_count < 1 || d->a0 + d->a_count > d->a_total || d->batch < 0 ||
+        d->chunks < 0 || (d->features && !d->full))
+        return fail(ctx, TT_ERR_INVALID, "bad plan descriptor");
+    if ((long long)d->a_count * n * (d->batch > 1 ? d->batch : 1) >= (1ll << 31))
+        return fail(ctx, TT_ERR_INVALID, "plan too large");
+    DeviceGuard guard(ctx->device);
+    auto p = new tt_plan;
+    p->ctx = ctx;
+    p->d = *d;
+    p->d.batch = d->batch > 1 ? d->batch : 1;
+    p->F = d->full ? tt::kNumF : 1;
+    tt::launch_structure(d->a_count, &p->units, &p->pair);
+    const int B = p->d.batch;
+    // chunks: >= ~1.6e7 unit-taps (~40 us of kernel) each so the per-chunk enqueue cost stays hidden,
+    // at most 32 (measured on C2: 5 chunks 1.28 ms, 24-32 chunks 1.24 ms; C1 best unchunked)
+    int ch = d->chunks;
+    if (ch == 0) ch = int(std::max(1LL, std::min(32LL, (long long)p->units * n * n / 16000000LL)));
+    p->chunks = B > 1 ? 1 : std::max(1, std::min(ch, p->units));
+    const std::size_t N2 = std::size_t(n) * n;
+    const std::size_t rows = std::size_t(B) * d->a_count;
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](auto** ptr, std::size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc((void**)ptr, bytes ? bytes : 4);
+    };
+    alloc(&p->img, B * N2 * 4);
+    alloc(&p->ctab, std::size_t(d->a_total) * 4);
+    alloc(&p->stab, std::size_t(d->a_total) * 4);
+    alloc(&p->out, rows * p->F * n * 4);
+    if (d->full) {
+        alloc(&p->wtab, std::size_t(n) * 32);
+        alloc(&p->wsoa, tt::weights_soa_bytes(n));
+        alloc(&p->med, rows * 2 * n * 4);
+    }
+    if (d->features) alloc(&p->circ, rows * tt::kNumF * 3 * 4);
+    for (cudaStream_t* s : {&p->sc[0], &p->sc[1], &p->sx})
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+    p->done.resize(p->chunks, nullptr);
+    for (auto& ev : p->done)
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->traced, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        plan_release(p);
+        return cuda_fail(ctx, e, "plan buffers");
+    }
+    // tables (host f64 -> f32, spec §2.1-2.2), the pass-2 weight layout, the image texture
+    std::vector<float> ct(d->a_total), st(d->a_total), wt(d->full ? std::size_t(n) * 8 : 0);
+    tt_make_tables(n, d->a_total, ct.data(), st.data(), d->full ? wt.data() : nullptr);
+    e = cudaMemcpyAsync(p->ctab, ct.data(), ct.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->stab, st.data(), st.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
+    if (e == cudaSuccess && d->full) {
+        e = cudaMemcpyAsync(p->wtab, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
+        if (e == cudaSuccess) e = tt::launch_weights_soa(p->wtab, n, p->wsoa, p->sc[0]);
+    }
+    if (e == cudaSuccess && ctx->sampler == int(tt::Sampler::Texture))
+        e = B > 1 ? tt::make_image_atlas(p->img, n, B, (long long)N2, p->sc[0], &p->arr, &p->tex, &p->cols)
+                  : tt::make_image_texture(p->img, n, p->sc[0], &p->arr, &p->tex);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->sc[0]);
+    if (e != cudaSuccess) {
+        plan_release(p);
+        return cuda_fail(ctx, e, "plan setup");
+    }
+    *out = p;
+    return TT_OK;
+}
+
+tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t* h_med, float* h_circ) {
+    if (!p || !h_img) return fail(p ? p->ctx : nullptr, TT_ERR_INVALID, "bad plan run arguments");
+    tt_ctx* ctx = p->ctx;
+    if (ctx->destroyed) return fail(ctx, TT_ERR_INVALID, "context destroyed");
+    DeviceGuard guard(ctx->device);
+    const tt_plan_desc& d = p->d;
+    const int n = d.n, B = d.batch, F = p->F;
+    const std::size_t N2 = std::size_t(n) * n;
+    const std::size_t row_f = std::size_t(F) * n, row_m = 2 * std::size_t(n);
+    cudaError_t e = cudaSuccess;
+    std::uint64_t h2d = 0, d2h = 0, launches = 0;
+    auto ok = [&](cudaError_t x) {
+        if (e == cudaSuccess) e = x;
+        return e == cudaSuccess;
+    };
+    // 1. image in (straight into the texture array when the sampler reads only the texture)
+    const bool tex = ctx->sampler == int(tt::Sampler::Texture);
+    if (tex && B == 1) {
+        ok(cudaMemcpy2DToArrayAsync(p->arr, 0, 0, h_img, std::size_t(n) * 4, std::size_t(n) * 4, std::size_t(n),
+                                    cudaMemcpyHostToDevice, p->sc[0]));
+    } else {
+        ok(cudaMemcpyAsync(p->img, h_img, B * N2 * 4, cudaMemcpyHostToDevice, p->sc[0]));
+        if (tex) {
+            ok(tt::fill_image_atlas(p->arr, p->img, n, B, (long long)N2, p->cols, p->sc[0]));
+            ++launches;
+        }
+    }
+    h2d += B * N2 * 4;
+    ok(cudaEventRecord(p->ready, p->sc[0]));
+    ok(cudaStreamWaitEvent(p->sc[1], p->ready, 0));
+    // 2. chunked fused kernel; each finished chunk's rows go out on the copy stream
+    for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
+        const int u0 = int((long long)p->units * c / p->chunks), u1 = int((long long)p->units * (c + 1) / p->chunks);
+        cudaStream_t s = p->sc[c & 1];
+        tt::TraceArgs ta;
+        ta.img = p->img;
+        ta.tex = p->tex;
+        ta.sampler = tex ? tt::Sampler::Texture : tt::Sampler::Global;
+        ta.atlas_cols = p->cols;
+        ta.n = n;
+        ta.a0 = d.a0 + u0;
+        ta.a_count = u1 - u0;
+        ta.pair_stride = p->pair;
+        ta.partner_row = p->units;
+        ta.ctab = p->ctab;
+        ta.stab = p->stab;
+        ta.wtab = p->wtab;
+        ta.wsoa = p->wsoa;
+        ta.out = p->out + std::size_t(u0) * row_f;
+        ta.med = d.full ? p->med + std::size_t(u0) * row_m : nullptr;
+        ta.full = d.full != 0;
+        ta.batch = B;
+        if (B > 1) ta.partner_row = -1;  // one launch over the batch: [b][rows] layout
+        if (!ok(tt::launch_trace(ta, s))) break;
+        launches += tt::trace_launch_count(ta);
+        ok(cudaEventRecord(p->done[c], s));
+        if (B == 1 && (h_out || h_med)) {
+            ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
+            const int cu = u1 - u0;
+            for (int half = 0; half < (p->pair ? 2 : 1); ++half) {  // forward rows, then the mirror rows
+                const std::size_t r0 = std::size_t(u0 + half * p->units);
+                if (h_out) {
+                    ok(cudaMemcpyAsync(h_out + r0 * row_f, p->out + r0 * row_f, cu * row_f * 4,
+                                       cudaMemcpyDeviceToHost, p->sx));
+                    d2h += cu * row_f * 4;
+                }
+                if (h_med && d.full) {
+                    ok(cudaMemcpyAsync(h_med + r0 * row_m, p->med + r0 * row_m, cu * row_m * 4,
+                                       cudaMemcpyDeviceToHost, p->sx));
+                    d2h += cu * row_m * 4;
+                }
+            }
+        }
+    }
+    // 3. batched runs download after the single launch; features over the whole sinogram
+    for (int c = 0; c < p->chunks; ++c) ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
+    const std::size_t rows = std::size_t(B) * d.a_count;
+    if (B > 1) {
+        if (h_out) {
+            ok(cudaMemcpyAsync(h_out, p->out, rows * row_f * 4, cudaMemcpyDeviceToHost, p->sx));
+            d2h += rows * row_f * 4;
+        }
+        if (h_med && d.full) {
+            ok(cudaMemcpyAsync(h_med, p->med, rows * row_m * 4, cudaMemcpyDeviceToHost, p->sx));
+            d2h += rows * row_m * 4;
+        }
+    }
+    if (d.features) {
+        ok(tt::launch_circus(p->out, n, int(rows * tt::kNumF), p->circ, p->sx));
+        ++launches;
+        if (h_circ) {
+            ok(cudaMemcpyAsync(h_circ, p->circ, rows * tt::kNumF * 3 * 4, cudaMemcpyDeviceToHost, p->sx));
+            d2h += rows * tt::kNumF * 3 * 4;
+        }
+    }
+    ok(cudaStreamSynchronize(p->sx));
+    ok(cudaStreamSynchronize(p->sc[0]));
+    ok(cudaStreamSynchronize(p->sc[1]));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "plan run");
+    ctx->c.bytes_h2d += h2d;
+    ctx->c.bytes_d2h += d2h;
+    ctx->c.gpu_kernel_launches += launches;
+    return TT_OK;
+}
+
+tt_status tt_plan_chunks(const tt_plan* p, int* chunks) {
+    if (!p || !chunks) return fail(nullptr, TT_ERR_INVALID, "null argument");
+    *chunks = p->chunks;
+    return TT_OK;
+}
+
+tt_status tt_plan_destroy(tt_plan* p) {
+    plan_release(p);
+    return TT_OK;
+}
+
+}  // extern "C"

@@ -180,6 +180,46 @@ class TraceTransform:
             self._res = None
 
 
+class Plan:
+    """Host-to-host pipelined form of the path (tt_plan_*): tables, texture and
+    outputs stay on the device; ``run`` uploads the image(s), runs the fused
+    kernel in angle chunks while finished chunks download (overlapped D2H), runs
+    the P-functional stage, and fills the given host arrays (pinned for overlap).
+    Outputs equal one whole launch bit-for-bit."""
+
+    def __init__(self, ctx: DeviceContext, n: int, angles: int, full: bool = True, a0: int = 0,
+                 a_count: int | None = None, features: bool = False, batch: int = 1, chunks: int = 0):
+        self.ctx, self.n, self.full, self.batch = ctx, n, full, batch
+        self.a_count = angles - a0 if a_count is None else a_count
+        self.features = features and full
+        d = _lib.PlanDesc(n, angles, a0, self.a_count, int(full), int(self.features), batch, chunks)
+        self._p = C.c_void_p()
+        _check(lib.tt_plan_create(ctx._p, C.byref(d), C.byref(self._p)), ctx._p)
+        c = C.c_int()
+        _check(lib.tt_plan_chunks(self._p, C.byref(c)))
+        self.chunks = c.value
+
+    def run(self, img, out=None, med=None, circ=None) -> None:
+        def ptr(a, dt):
+            if a is None:
+                return None
+            assert a.dtype == dt and a.flags["C_CONTIGUOUS"]
+            return C.c_void_p(a.ctypes.data)
+        F = NF if self.full else 1
+        lead = self.batch * self.a_count
+        for a, size in ((out, lead * F * self.n), (med, lead * 2 * self.n), (circ, lead * NF * 3)):
+            assert a is None or a.size == size, "output array has the wrong size"
+        assert img.size == self.batch * self.n * self.n
+        _check(lib.tt_plan_run(self._p, ptr(img, np.float32), ptr(out, np.float32),
+                               ptr(med if self.full else None, np.int32), ptr(circ if self.features else None,
+                                                                                np.float32)), self.ctx._p)
+
+    def destroy(self) -> None:
+        if self._p:
+            lib.tt_plan_destroy(self._p)
+            self._p = C.c_void_p()
+
+
 def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, stab_ptr: int, wtab_ptr: int,
                  out_ptr: int, med_ptr: int = 0, full: bool = True, sampler: int = 0, stream: int = 0,
                  tex=None, pair_stride: int = 0, batch: int = 1, img_stride: int = 0, wsoa_ptr: int = 0) -> None:

@@ -1,0 +1,90 @@
+"""Pipelined host-to-host plans (tt_plan_*): chunked launches with overlapped
+downloads must reproduce the single-launch drop-in path bit-for-bit."""
+import numpy as np
+import pytest
+
+import paper_1604_03410_b200 as tt
+from paper_1604_03410_b200.trace import NF
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx(gpu):
+    c = tt.create_context(gpu)
+    yield c
+    c.destroy()
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+@pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
+@pytest.mark.parametrize("n,A,full,chunks", [(256, 360, True, 0), (256, 360, True, 7), (1000, 12, True, 5),
+                                             (128, 9, True, 3), (64, 10, False, 4), (1024, 16, True, 8)])
+def test_plan_equals_one_launch(ctx, n, A, full, chunks, sampler):
+    ctx.set_sampler(sampler)
+    img = tt.synth_image(tt.PHANTOM, n)
+    ref_out, ref_med, rep = tt.TraceTransform(ctx, n, A, full=full)(img)
+    assert rep.ok()
+    plan = tt.Plan(ctx, n, A, full=full, features=full, chunks=chunks)
+    F = NF if full else 1
+    out = np.full((A, F, n), np.nan, np.float32)
+    med = np.full((A, 2, n), -7, np.int32) if full else None
+    circ = np.zeros((A, NF, 3), np.float32) if full else None
+    for _ in range(2):  # reusable
+        plan.run(img, out, med, circ)
+    assert np.array_equal(_bits(out), _bits(ref_out))
+    if full:
+        assert np.array_equal(med, ref_med)
+        assert np.array_equal(_bits(circ), _bits(tt.circus(ctx, ref_out)))
+    plan.destroy()
+
+
+def test_plan_angle_range_and_partial_outputs(ctx):
+    n, A, a0, cnt = 256, 40, 6, 20
+    img = tt.synth_image(tt.DISK, n)
+    ref_out, ref_med, _ = tt.TraceTransform(ctx, n, A, a0=a0, a_count=cnt)(img)
+    plan = tt.Plan(ctx, n, A, a0=a0, a_count=cnt, chunks=3)
+    out = np.empty((cnt, NF, n), np.float32)
+    plan.run(img, out)  # medians and features not requested
+    assert np.array_equal(_bits(out), _bits(ref_out))
+    plan.destroy()
+
+
+def test_plan_batched_features(ctx):
+    n, A, B = 128, 12, 3
+    imgs = np.stack([tt.synth_image(tt.DISK, n, tt.SEEDS[tt.DISK] + b) for b in range(B)])
+    plan = tt.Plan(ctx, n, A, features=True, batch=B)
+    out = np.empty((B, A, NF, n), np.float32)
+    med = np.empty((B, A, 2, n), np.int32)
+    circ = np.empty((B, A, NF, 3), np.float32)
+    plan.run(imgs, out, med, circ)
+    for b in range(B):
+        ro, rm, _ = tt.TraceTransform(ctx, n, A)(imgs[b])
+        assert np.array_equal(_bits(out[b]), _bits(ro)) and np.array_equal(med[b], rm)
+        assert np.array_equal(_bits(circ[b]), _bits(tt.circus(ctx, ro)))
+    plan.destroy()
+
+
+def test_plan_counts_bytes_and_launches(ctx):
+    n, A = 256, 24
+    plan = tt.Plan(ctx, n, A, chunks=4)
+    c0 = ctx.counters()
+    out = np.empty((A, NF, n), np.float32)
+    plan.run(tt.synth_image(tt.DISK, n), out)
+    c1 = ctx.counters()
+    assert c1["bytes_h2d"] - c0["bytes_h2d"] == n * n * 4
+    assert c1["bytes_d2h"] - c0["bytes_d2h"] == out.nbytes
+    assert c1["gpu_kernel_launches"] - c0["gpu_kernel_launches"] == plan.chunks == 4
+    plan.destroy()
+
+
+def test_plan_rejects_bad_descriptors(ctx):
+    with pytest.raises(Exception):
+        tt.Plan(ctx, 0, 10)
+    with pytest.raises(Exception):
+        tt.Plan(ctx, 64, 10, a0=5, a_count=10)
+    with pytest.raises(Exception):
+        tt.Plan(ctx, 64, 0)
