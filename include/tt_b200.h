@@ -202,9 +202,9 @@ tt_status tt_make_tables(int n, int a_total, float* ctab, float* stab, float* wt
 /* Deterministic synthetic images: kind 0 disk-noise, 1 phantom, 2 sparse. */
 tt_status tt_synth_image(int kind, uint64_t seed, int n, float* img);
 /* Slots (lanes) per line of the fused kernel for side n: 8, 16 or 32 (one
- * warp segment) or 32W (W warps) -- the reduction schedule the replay oracle
- * mirrors. */
-int tt_schedule_slots(int n);
+ * warp segment) or 32W (W warps); T0-only (full = 0) launches with n > 1024
+ * use 32 -- the reduction schedule the replay oracle mirrors. */
+int tt_schedule_slots(int n, int full);
 /* Largest n the fused T0..T5 kernel supports. */
 int tt_max_full_n(void);
 

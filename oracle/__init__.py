@@ -49,7 +49,7 @@ def lib():
         L.tto_tables.argtypes = [ctypes.c_int, ctypes.c_int, fp, fp, fp]
         L.tto_synth.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, fp]
         L.tto_line_samples.argtypes = [fp, ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_int, fp]
-        L.tto_schedule_slots.argtypes = [ctypes.c_int]
+        L.tto_schedule_slots.argtypes = [ctypes.c_int, ctypes.c_int]
         L.tto_schedule_slots.restype = ctypes.c_int
         L.tto_transform.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, ip, dp, dp, ctypes.c_int]
@@ -88,9 +88,9 @@ def synth(kind: int, n: int, seed: int | None = None) -> np.ndarray:
     return img
 
 
-def schedule_slots(n: int) -> int:
-    """Slots (lanes) per line of the B200 kernel for side n (8/16/32 or 32W)."""
-    return lib().tto_schedule_slots(n)
+def schedule_slots(n: int, full: bool = True) -> int:
+    """Slots (lanes) per line of the B200 kernel for side n (8/16/32 or 32W; T0 only, n > 1024: 32)."""
+    return lib().tto_schedule_slots(n, int(full))
 
 
 def line_samples(img, n, c, s, p):

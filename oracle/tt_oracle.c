@@ -145,8 +145,9 @@ void tto_line_samples(const float* img, int n, float c, float s, int p, float* v
  * slots per line NS.  n <= 1024: one segment of 8, 16 or 32 lanes (the
  * smallest with ceil(n/NS) <= 32; sub-warp segments need 32/NS | n, else 32);
  * larger n: 32W lanes, W the smallest power of two with ceil(n/32W) <= 32,
- * at most 16. */
-int tto_schedule_slots(int n) {
+ * at most 16; T0-only (full = 0) with n > 1024: 32 (one warp per line). */
+int tto_schedule_slots(int n, int full) {
+    if (!full && n > 1024) return 32;
     if (n <= 1024) {
         int seg = 8;
         while (seg < 32 && (n + seg - 1) / seg > 32) seg *= 2;
@@ -450,7 +451,7 @@ static void replay_unit(const float* img, int n, int a0, int units, int pair_str
 void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stride, const float* ctab,
                        const float* stab, const float* wtab, int full, int NS, float* out, int32_t* med,
                        int nthreads) {
-    if (NS <= 0) NS = tto_schedule_slots(n);
+    if (NS <= 0) NS = tto_schedule_slots(n, full);
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #else
@@ -487,7 +488,7 @@ void tto_transform(const float* img, int n, int a0, int a_count, int a_total, co
                    double* out64, double* absm, int nthreads) {
     (void)a_total;
     const int F = full ? TTO_NF : 1;
-    if (W <= 0) W = tto_schedule_slots(n);
+    if (W <= 0) W = tto_schedule_slots(n, full);
     if (mode == TTO_REPLAY) {
         int units, stride;
         tto_launch_structure(a_count, &units, &stride);
@@ -618,7 +619,7 @@ long tto_check(const float* img, int n, int a0, int a_count, int a_total, const 
                double chain, double* stats, int nthreads) {
     (void)a_total;
     const int F = full ? TTO_NF : 1;
-    const int NS = W > 0 ? W : tto_schedule_slots(n);
+    const int NS = W > 0 ? W : tto_schedule_slots(n, 1);
     const int K = (n + NS - 1) / NS;
     /* fp32 chain length of the GPU schedule: slot partial + butterfly + groups
      * (callers checking a sequential fp32 result pass chain = n) */

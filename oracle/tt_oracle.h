@@ -58,7 +58,7 @@ void tto_line_samples(const float* img, int n, float c, float s, int p, float* v
 
 /* Slots (lanes) per line the B200 kernel uses for side n: the replay schedule
  * (8/16/32: one warp segment; 32W: W warps). */
-int tto_schedule_slots(int n);
+int tto_schedule_slots(int n, int full);
 
 /*
  * Whole transform over angles [a0, a0+a_count) of a_total.

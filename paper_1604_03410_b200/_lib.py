@@ -93,7 +93,7 @@ _sigs = {
     "tt_events": (_S, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "tt_make_tables": (_S, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tt_synth_image": (_S, [C.c_int, C.c_uint64, C.c_int, C.c_void_p]),
-    "tt_schedule_slots": (C.c_int, [C.c_int]),
+    "tt_schedule_slots": (C.c_int, [C.c_int, C.c_int]),
     "tt_max_full_n": (C.c_int, []),
     "tt_count_inbounds_taps": (C.c_uint64, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_ffma_probe": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),

@@ -1086,7 +1086,7 @@ tt_status tt_events(tt_ctx* ctx, std::uint8_t* buf, std::size_t cap, std::size_t
 
 // ---- trace-transform helpers -------------------------------------------------
 
-int tt_schedule_slots(int n) { return tt::schedule_slots(n); }
+int tt_schedule_slots(int n, int full) { return tt::schedule_slots(n, full != 0); }
 
 tt_status tt_ffma_probe(float* d_out, int blocks, int iters, void* stream) {
     if (!d_out || blocks < 1 || iters < 1) return fail(nullptr, TT_ERR_INVALID, "bad probe arguments");

@@ -44,9 +44,9 @@ struct TraceArgs {
 };
 
 // Slots (lanes) per line of the fused kernel for side n: 8/16/32 (one warp
-// segment) or 32W (W warps) -- the reduction schedule that oracle/tt_oracle.c
-// TTO_REPLAY mirrors.
-int schedule_slots(int n);
+// segment) or 32W (W warps); T0-only launches with n > 1024 use 32 -- the
+// reduction schedule that oracle/tt_oracle.c TTO_REPLAY mirrors.
+int schedule_slots(int n, bool full = true);
 
 // Launch units for a drop-in launch of a_count angles: pairs (i, i+a_count/2)
 // when a_count is even (the kernel pairs mirrored angles).

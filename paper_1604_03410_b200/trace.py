@@ -42,9 +42,9 @@ def synth_image(kind: int, n: int, seed: int | None = None) -> np.ndarray:
     return img
 
 
-def schedule_slots(n: int) -> int:
-    """Slots (lanes) per line of the fused kernel: 8/16/32 (warp segment) or 32W."""
-    return lib.tt_schedule_slots(n)
+def schedule_slots(n: int, full: bool = True) -> int:
+    """Slots (lanes) per line of the fused kernel: 8/16/32 (warp segment) or 32W (T0 only, n > 1024: 32)."""
+    return lib.tt_schedule_slots(n, int(full))
 
 
 def max_full_n() -> int:

@@ -53,7 +53,8 @@ def test_synthetic_images_bit_identical_to_oracle(kind, n):
 
 def test_schedule_matches_oracle_replay_schedule():
     for n in (1, 2, 16, 64, 100, 101, 255, 256, 300, 512, 777, 1000, 1024, 1500, 2048, 4095, 4096, 8192, 16384):
-        assert tt.schedule_slots(n) == O.schedule_slots(n)
+        for full in (True, False):
+            assert tt.schedule_slots(n, full) == O.schedule_slots(n, full)
 
 
 def test_no_gpu_fails_loudly():

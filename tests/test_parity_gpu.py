@@ -56,7 +56,8 @@ def test_fused_t05_bit_exact_vs_replay_and_within_tolerance_of_f64(ctx, n, A, ki
 
 @pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
 @pytest.mark.parametrize("n,A,kind", [(64, 12, tt.DISK), (256, 360, tt.PHANTOM), (777, 5, tt.SPARSE),
-                                      (4096, 2, tt.DISK), (20000, 1, tt.DISK)])
+                                      (1025, 4, tt.PHANTOM), (2048, 6, tt.PHANTOM), (4096, 2, tt.DISK),
+                                      (8192, 2, tt.SPARSE), (20000, 1, tt.DISK)])
 def test_radon_t0_bit_exact(ctx, n, A, kind, sampler):
     img = tt.synth_image(kind, n)
     tr, out, _ = _run(ctx, img, n, A, full=False, sampler=sampler)
