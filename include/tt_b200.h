@@ -276,10 +276,12 @@ tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, voi
 /* ---- plans: the host-to-host form of the path -------------------------------
  * One plan = one (n, angles, functionals, batch) configuration with its device
  * tables, image texture and output buffers resident.  tt_plan_run uploads the
- * image(s), runs the fused kernel in `chunks` angle chunks over two compute
+ * image, runs the fused kernel in `chunks` angle chunks over two compute
  * streams while a copy stream downloads each finished chunk's rows (overlapped
  * D2H), runs the P-functional stage once over the sinogram, and returns when
- * every requested host buffer is filled.  Results equal one whole launch
+ * every requested host buffer is filled.  Batched plans chunk by images
+ * instead: chunk c uploads while chunk c-1 computes (trace + features) and
+ * chunk c-2 downloads.  Results equal one whole launch
  * bit-for-bit.  Host buffers should be pinned (tt_host_alloc) for the copies to
  * overlap.  The caller-side flow this replaces is cuda_launch's
  * marshal -> launch -> download sequence (autolaunch.hpp:167-245) repeated per
@@ -293,7 +295,8 @@ typedef struct tt_plan_desc {
     int32_t full;     /* 1: T0..T5 (+ medians), 0: T0 (Radon) only */
     int32_t features; /* 1: P-functionals (circus) after the trace (full only) */
     int32_t batch;    /* images per run (0 or 1: one) */
-    int32_t chunks;   /* pipeline chunks (0: automatic; batched plans use 1) */
+    int32_t chunks;   /* pipeline chunks: angle chunks (one image) or image chunks (batch);
+                         0 = automatic */
 } tt_plan_desc;
 tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out);
 /* h_img [batch][n][n]; h_out [batch][a_count][F][n], h_med [batch][a_count][2][n],

@@ -1300,8 +1300,9 @@ struct tt_plan {
     cudaArray_t arr = nullptr;
     cudaTextureObject_t tex = 0;
     int cols = 1;
-    cudaStream_t sc[2] = {nullptr, nullptr}, sx = nullptr;
-    std::vector<cudaEvent_t> done;  // per chunk: its rows are final
+    cudaStream_t sc[2] = {nullptr, nullptr}, sx = nullptr, si = nullptr;
+    std::vector<cudaEvent_t> done;      // per chunk: its rows are final
+    std::vector<cudaEvent_t> uploaded;  // per chunk (batched plans): its images are on the device
     cudaEvent_t ready = nullptr, traced = nullptr;
 };
 
@@ -1310,9 +1311,10 @@ namespace {
 void plan_release(tt_plan* p) {
     if (!p) return;
     DeviceGuard guard(p->ctx->device);
-    for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx})
+    for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx, p->si})
         if (s) cudaStreamSynchronize(s);
     for (cudaEvent_t e : p->done) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->uploaded) cudaEventDestroy(e);
     if (p->ready) cudaEventDestroy(p->ready);
     if (p->traced) cudaEventDestroy(p->traced);
     if (p->tex) cudaDestroyTextureObject(p->tex);
@@ -1320,7 +1322,7 @@ void plan_release(tt_plan* p) {
     for (void* b : {(void*)p->img, (void*)p->ctab, (void*)p->stab, (void*)p->wtab, (void*)p->wsoa, (void*)p->out,
                     (void*)p->circ, (void*)p->med})
         if (b) cudaFree(b);
-    for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx})
+    for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx, p->si})
         if (s) cudaStreamDestroy(s);
     delete p;
 }
@@ -1351,8 +1353,8 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
     // chunks: >= ~1.6e7 unit-taps (~40 us of kernel) each so the per-chunk enqueue cost stays hidden,
     // at most 32 (measured on C2: 5 chunks 1.28 ms, 24-32 chunks 1.24 ms; C1 best unchunked)
     int ch = d->chunks;
-    if (ch == 0) ch = int(std::max(1LL, std::min(32LL, (long long)p->units * n * n / 16000000LL)));
-    p->chunks = B > 1 ? 1 : std::max(1, std::min(ch, p->units));
+    if (ch == 0) ch = int(std::max(1LL, std::min(32LL, (long long)p->units * B * n * n / 16000000LL)));
+    p->chunks = std::max(1, std::min(ch, B > 1 ? B : p->units));  // angle chunks (one image) or image chunks
     const std::size_t N2 = std::size_t(n) * n;
     const std::size_t rows = std::size_t(B) * d->a_count;
     cudaError_t e = cudaSuccess;
@@ -1369,11 +1371,13 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
         alloc(&p->med, rows * 2 * n * 4);
     }
     if (d->features) alloc(&p->circ, rows * tt::kNumF * 3 * 4);
-    for (cudaStream_t* s : {&p->sc[0], &p->sc[1], &p->sx})
+    for (cudaStream_t* s : {&p->sc[0], &p->sc[1], &p->sx, &p->si})
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
     p->done.resize(p->chunks, nullptr);
-    for (auto& ev : p->done)
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    p->uploaded.resize(p->chunks, nullptr);
+    for (auto* evs : {&p->done, &p->uploaded})
+        for (auto& ev : *evs)
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->traced, cudaEventDisableTiming);
     if (e != cudaSuccess) {
@@ -1409,32 +1413,15 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
     const tt_plan_desc& d = p->d;
     const int n = d.n, B = d.batch, F = p->F;
     const std::size_t N2 = std::size_t(n) * n;
-    const std::size_t row_f = std::size_t(F) * n, row_m = 2 * std::size_t(n);
+    const std::size_t row_f = std::size_t(F) * n, row_m = 2 * std::size_t(n), row_c = std::size_t(tt::kNumF) * 3;
     cudaError_t e = cudaSuccess;
     std::uint64_t h2d = 0, d2h = 0, launches = 0;
     auto ok = [&](cudaError_t x) {
         if (e == cudaSuccess) e = x;
         return e == cudaSuccess;
     };
-    // 1. image in (straight into the texture array when the sampler reads only the texture)
     const bool tex = ctx->sampler == int(tt::Sampler::Texture);
-    if (tex && B == 1) {
-        ok(cudaMemcpy2DToArrayAsync(p->arr, 0, 0, h_img, std::size_t(n) * 4, std::size_t(n) * 4, std::size_t(n),
-                                    cudaMemcpyHostToDevice, p->sc[0]));
-    } else {
-        ok(cudaMemcpyAsync(p->img, h_img, B * N2 * 4, cudaMemcpyHostToDevice, p->sc[0]));
-        if (tex) {
-            ok(tt::fill_image_atlas(p->arr, p->img, n, B, (long long)N2, p->cols, p->sc[0]));
-            ++launches;
-        }
-    }
-    h2d += B * N2 * 4;
-    ok(cudaEventRecord(p->ready, p->sc[0]));
-    ok(cudaStreamWaitEvent(p->sc[1], p->ready, 0));
-    // 2. chunked fused kernel; each finished chunk's rows go out on the copy stream
-    for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
-        const int u0 = int((long long)p->units * c / p->chunks), u1 = int((long long)p->units * (c + 1) / p->chunks);
-        cudaStream_t s = p->sc[c & 1];
+    auto trace_args = [&](int u0, int u1, int b0, int b1) {
         tt::TraceArgs ta;
         ta.img = p->img;
         ta.tex = p->tex;
@@ -1444,59 +1431,99 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
         ta.a0 = d.a0 + u0;
         ta.a_count = u1 - u0;
         ta.pair_stride = p->pair;
-        ta.partner_row = p->units;
+        ta.partner_row = B == 1 ? p->units : -1;  // angle chunks write their mirror rows at U (one image)
         ta.ctab = p->ctab;
         ta.stab = p->stab;
         ta.wtab = p->wtab;
         ta.wsoa = p->wsoa;
-        ta.out = p->out + std::size_t(u0) * row_f;
-        ta.med = d.full ? p->med + std::size_t(u0) * row_m : nullptr;
+        const std::size_t rows0 = std::size_t(b0) * d.a_count + u0;  // first output row of the launch
+        ta.out = p->out + rows0 * row_f;
+        ta.med = d.full ? p->med + rows0 * row_m : nullptr;
         ta.full = d.full != 0;
-        ta.batch = B;
-        if (B > 1) ta.partner_row = -1;  // one launch over the batch: [b][rows] layout
-        if (!ok(tt::launch_trace(ta, s))) break;
-        launches += tt::trace_launch_count(ta);
-        ok(cudaEventRecord(p->done[c], s));
-        if (B == 1 && (h_out || h_med)) {
+        ta.batch = b1 - b0;
+        ta.img0 = b0;
+        return ta;
+    };
+    auto download = [&](std::size_t r0, std::size_t cnt) {  // output rows [r0, r0 + cnt) on the copy stream
+        if (h_out) {
+            ok(cudaMemcpyAsync(h_out + r0 * row_f, p->out + r0 * row_f, cnt * row_f * 4, cudaMemcpyDeviceToHost, p->sx));
+            d2h += cnt * row_f * 4;
+        }
+        if (h_med && d.full) {
+            ok(cudaMemcpyAsync(h_med + r0 * row_m, p->med + r0 * row_m, cnt * row_m * 4, cudaMemcpyDeviceToHost, p->sx));
+            d2h += cnt * row_m * 4;
+        }
+    };
+    if (B == 1) {
+        // 1. image in (straight into the texture array when the sampler reads only the texture)
+        if (tex)
+            ok(cudaMemcpy2DToArrayAsync(p->arr, 0, 0, h_img, std::size_t(n) * 4, std::size_t(n) * 4, std::size_t(n),
+                                        cudaMemcpyHostToDevice, p->sc[0]));
+        else
+            ok(cudaMemcpyAsync(p->img, h_img, N2 * 4, cudaMemcpyHostToDevice, p->sc[0]));
+        h2d += N2 * 4;
+        ok(cudaEventRecord(p->ready, p->sc[0]));
+        ok(cudaStreamWaitEvent(p->sc[1], p->ready, 0));
+        // 2. angle chunks alternating over two compute streams; each finished chunk's forward and
+        //    mirror rows go out on the copy stream while later chunks compute
+        for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
+            const int u0 = int((long long)p->units * c / p->chunks), u1 = int((long long)p->units * (c + 1) / p->chunks);
+            cudaStream_t s = p->sc[c & 1];
+            tt::TraceArgs ta = trace_args(u0, u1, 0, 1);
+            if (!ok(tt::launch_trace(ta, s))) break;
+            launches += tt::trace_launch_count(ta);
+            ok(cudaEventRecord(p->done[c], s));
+            if (h_out || h_med) {
+                ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
+                for (int half = 0; half < (p->pair ? 2 : 1); ++half) download(std::size_t(u0 + half * p->units), u1 - u0);
+            }
+        }
+        for (int c = 0; c < p->chunks; ++c) ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
+        if (d.features) {  // 3. P-functionals over the whole sinogram
+            const std::size_t rows = d.a_count;
+            ok(tt::launch_circus(p->out, n, int(rows * tt::kNumF), p->circ, p->sx));
+            ++launches;
+            if (h_circ) {
+                ok(cudaMemcpyAsync(h_circ, p->circ, rows * row_c * 4, cudaMemcpyDeviceToHost, p->sx));
+                d2h += rows * row_c * 4;
+            }
+        }
+    } else {
+        // Image chunks: chunk c's upload (copy-in stream) overlaps chunk c-1's trace + features
+        // (compute stream) and chunk c-2's download (copy-out stream).
+        const int units_all = d.a_count;  // rows per image
+        for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
+            const int b0 = int((long long)B * c / p->chunks), b1 = int((long long)B * (c + 1) / p->chunks);
+            const std::size_t cnt = std::size_t(b1 - b0);
+            ok(cudaMemcpyAsync(p->img + b0 * N2, h_img + b0 * N2, cnt * N2 * 4, cudaMemcpyHostToDevice, p->si));
+            h2d += cnt * N2 * 4;
+            ok(cudaEventRecord(p->uploaded[c], p->si));
+            cudaStream_t s = p->sc[0];
+            ok(cudaStreamWaitEvent(s, p->uploaded[c], 0));
+            if (tex) {
+                ok(tt::fill_image_atlas(p->arr, p->img + b0 * N2, n, int(cnt), (long long)N2, p->cols, s, b0));
+                ++launches;
+            }
+            tt::TraceArgs ta = trace_args(0, p->units, b0, b1);
+            if (!ok(tt::launch_trace(ta, s))) break;
+            launches += tt::trace_launch_count(ta);
+            const std::size_t r0 = std::size_t(b0) * units_all, rows = cnt * units_all;
+            if (d.features) {
+                ok(tt::launch_circus(p->out + r0 * row_f, n, int(rows * tt::kNumF), p->circ + r0 * row_c, s));
+                ++launches;
+            }
+            ok(cudaEventRecord(p->done[c], s));
             ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
-            const int cu = u1 - u0;
-            for (int half = 0; half < (p->pair ? 2 : 1); ++half) {  // forward rows, then the mirror rows
-                const std::size_t r0 = std::size_t(u0 + half * p->units);
-                if (h_out) {
-                    ok(cudaMemcpyAsync(h_out + r0 * row_f, p->out + r0 * row_f, cu * row_f * 4,
-                                       cudaMemcpyDeviceToHost, p->sx));
-                    d2h += cu * row_f * 4;
-                }
-                if (h_med && d.full) {
-                    ok(cudaMemcpyAsync(h_med + r0 * row_m, p->med + r0 * row_m, cu * row_m * 4,
-                                       cudaMemcpyDeviceToHost, p->sx));
-                    d2h += cu * row_m * 4;
-                }
+            download(r0, rows);
+            if (d.features && h_circ) {
+                ok(cudaMemcpyAsync(h_circ + r0 * row_c, p->circ + r0 * row_c, rows * row_c * 4, cudaMemcpyDeviceToHost,
+                                   p->sx));
+                d2h += rows * row_c * 4;
             }
         }
     }
-    // 3. batched runs download after the single launch; features over the whole sinogram
-    for (int c = 0; c < p->chunks; ++c) ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
-    const std::size_t rows = std::size_t(B) * d.a_count;
-    if (B > 1) {
-        if (h_out) {
-            ok(cudaMemcpyAsync(h_out, p->out, rows * row_f * 4, cudaMemcpyDeviceToHost, p->sx));
-            d2h += rows * row_f * 4;
-        }
-        if (h_med && d.full) {
-            ok(cudaMemcpyAsync(h_med, p->med, rows * row_m * 4, cudaMemcpyDeviceToHost, p->sx));
-            d2h += rows * row_m * 4;
-        }
-    }
-    if (d.features) {
-        ok(tt::launch_circus(p->out, n, int(rows * tt::kNumF), p->circ, p->sx));
-        ++launches;
-        if (h_circ) {
-            ok(cudaMemcpyAsync(h_circ, p->circ, rows * tt::kNumF * 3 * 4, cudaMemcpyDeviceToHost, p->sx));
-            d2h += rows * tt::kNumF * 3 * 4;
-        }
-    }
     ok(cudaStreamSynchronize(p->sx));
+    ok(cudaStreamSynchronize(p->si));
     ok(cudaStreamSynchronize(p->sc[0]));
     ok(cudaStreamSynchronize(p->sc[1]));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "plan run");

@@ -39,6 +39,7 @@ struct TraceArgs {
     bool full = true;             // T0..T5 (else T0 / Radon only)
     Sampler sampler = Sampler::Global;
     int batch = 1;                // images in this launch (same n, same angles)
+    int img0 = 0;                 // atlas/array index of the launch's first image (outputs stay launch-relative)
     long long img_stride = 0;     // elements between images (0: n*n) -- Global sampler
     int atlas_cols = 1;           // texture atlas tiles per row -- Texture sampler
 };
@@ -108,9 +109,10 @@ cudaError_t launch_circus(const float* sino, int n, int rows, float* circ, cudaS
 cudaError_t make_image_atlas(const float* imgs, int n, int batch, long long stride, cudaStream_t s, cudaArray_t* arr,
                              cudaTextureObject_t* tex, int* cols);
 
-// Refill an atlas created by make_image_atlas (stream-ordered).
+// Refill images [b0, b0 + batch) of an atlas created by make_image_atlas from
+// imgs (image b0 first; stream-ordered).
 cudaError_t fill_image_atlas(cudaArray_t arr, const float* imgs, int n, int batch, long long stride, int cols,
-                             cudaStream_t s);
+                             cudaStream_t s, int b0 = 0);
 
 // Writes a buffer larger than L2 (timing hygiene between bench iterations).
 cudaError_t launch_l2_flush(void* buf, uint64_t bytes, cudaStream_t s);

@@ -53,10 +53,13 @@ def test_plan_angle_range_and_partial_outputs(ctx):
     plan.destroy()
 
 
-def test_plan_batched_features(ctx):
+@pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
+@pytest.mark.parametrize("chunks", [0, 2, 3])
+def test_plan_batched_features(ctx, chunks, sampler):
+    ctx.set_sampler(sampler)
     n, A, B = 128, 12, 3
     imgs = np.stack([tt.synth_image(tt.DISK, n, tt.SEEDS[tt.DISK] + b) for b in range(B)])
-    plan = tt.Plan(ctx, n, A, features=True, batch=B)
+    plan = tt.Plan(ctx, n, A, features=True, batch=B, chunks=chunks)
     out = np.empty((B, A, NF, n), np.float32)
     med = np.empty((B, A, 2, n), np.int32)
     circ = np.empty((B, A, NF, 3), np.float32)
