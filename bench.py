@@ -184,11 +184,16 @@ def run_ours(args, ws, rank, local):
     from paper_1604_03410_b200._lib import lib
     from paper_1604_03410_b200.trace import image_atlas, image_texture, image_texture_destroy, image_texture_update
 
+    if args.dev_one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dev_one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = WORKLOADS[args.workload]
     n, A, full, feats_on = wl["n"], wl["angles"], wl["full"], wl["features"]
     F = 6 if full else 1
@@ -220,8 +225,11 @@ def run_ours(args, ws, rank, local):
         circ = torch.empty((B, a_cnt, F, 3), device="cuda")
         flush = torch.empty(int(256 << 20) // 4, device="cuda")  # > 126 MB L2
         wsoa = torch.empty(6 * n, device="cuda") if full else None  # pass-2 weight layout (constant of n)
-        gathered = torch.empty((A, F, n), device="cuda") if orient else None
-        gathered_raw = torch.empty((ws * a_cnt, F, n), device="cuda") if orient else None
+        # orientation shards: rank 0 holds the assembled sinogram (+ medians); every rank's fused
+        # kernel writes its rows straight into it over NVLink P2P (CUDA IPC mapping)
+        gathered = torch.empty((A, F, n), device="cuda") if orient and rank == 0 else None
+        gmed = torch.empty((A, 2, n), dtype=torch.int32, device="cuda") if orient and rank == 0 else None
+        signal = torch.zeros(1, device="cuda") if orient else None
         feats = torch.empty((ws * B, a_cnt, F, 3), device="cuda") if (ws > 1 and not orient) else None
     tex = None
     if args.sampler == 1:  # texture layout of this step's image(s); refreshed inside every timed step
@@ -230,12 +238,21 @@ def run_ours(args, ws, rank, local):
         tt.weights_soa(wtab.data_ptr(), n, wsoa.data_ptr(), sptr)
     launches_per_step = 1 + (1 if feats_on else 0) + (1 if tex is not None and B > 1 else 0)
 
+    close_peer = None
+    if orient:
+        peer, close_peer = shard.share_device_buffers(
+            [gathered.data_ptr(), gmed.data_ptr()] if rank == 0 else [], dist, local)
+        _, _, _, row0, prow = shard.direct_shard_rows(A, ws, rank, F, n)
+        out_ptr, med_ptr = peer[0] + row0 * F * n * 4, peer[1] + row0 * 2 * n * 4
+    else:
+        out_ptr, med_ptr, prow = out.data_ptr(), med.data_ptr(), 0
+
     def step():
         if tex is not None:
             image_texture_update(tex, img.data_ptr(), 0, sptr)
         tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
-                        out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
-                        pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0)
+                        out_ptr, med_ptr, full=full, sampler=args.sampler, stream=sptr, tex=tex,
+                        pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0, partner_row=prow)
 
     def features():
         if feats_on:  # P-functional (circus) stage consuming the sinograms
@@ -245,8 +262,8 @@ def run_ours(args, ws, rank, local):
         if not dist:
             return
         with torch.cuda.stream(stream):
-            if orient:  # the single NCCL gather of sinogram slices (equal shards: (A/2) % ws == 0)
-                shard.gather_sinograms(out[0], A, dist, out=gathered, raw=gathered_raw)
+            if orient:  # rows already written into rank 0's sinogram by the kernels: 4-byte completion signal
+                dist.all_reduce(signal)
             else:       # image sharding: gather the per-image circus features
                 dist.all_gather_into_tensor(feats, circ)
 
@@ -332,8 +349,22 @@ def run_ours(args, ws, rank, local):
            "ms_per_step": e2e_s * 1e3,
            "api": f"tt.Plan.run -> tt_plan_run (pinned H2D, {plan.chunks} chunked fused-kernel launches with "
                   "overlapped D2H of finished rows" + (", circus" if feats_on else "") + ")"}
-    # parity spot check of the e2e output against the device-resident one
-    if want_sino and not orient:
+    # parity spot checks: the e2e output against the device-resident one; under orientation
+    # sharding, rank 0's P2P-assembled sinogram against one whole single-GPU launch
+    if orient:
+        same = True
+        if rank == 0:
+            ref = torch.empty((A, F, n), device="cuda")
+            rmed = torch.empty((A, 2, n), dtype=torch.int32, device="cuda")
+            tt.trace_device(img.data_ptr(), n, 0, A, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
+                            ref.data_ptr(), rmed.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
+                            wsoa_ptr=wsoa.data_ptr() if full else 0)
+            torch.cuda.synchronize()
+            same = bool(torch.equal(gathered.view(torch.int32), ref.view(torch.int32)) and torch.equal(gmed, rmed))
+            del ref, rmed
+        dist.barrier()
+        close_peer()
+    elif want_sino:
         same = np.array_equal(h_out.reshape(out.shape), out.cpu().numpy())
     else:
         same = np.array_equal(h_circ.reshape(circ.shape), circ.cpu().numpy())
@@ -369,12 +400,16 @@ def run_ours(args, ws, rank, local):
                        "images": batch_total if images else (1 if orient else ws),
                        "functionals": ("T0-T5" if full else "T0") + (" + P1-P3 circus" if feats_on else ""),
                        "sampler": ["ldg", "tex"][args.sampler],
-                       "parallelism": (f"orientations sharded x{ws} + NCCL all_gather" if orient else
+                       "parallelism": (f"orientations sharded x{ws}; fused kernels write sinogram rows into "
+                                       "rank 0 over NVLink P2P + 4-byte NCCL completion signal" if orient else
                                        (f"images sharded x{ws} + NCCL feature gather" if ws > 1 else "1 GPU")),
                        "l2": "flushed (256 MiB memset) between timed steps",
                        "ms_per_image": ms_per_step / (batch_total if images else 1)},
             "e2e": e2e, "roofline": roofline, "clocks": clocks.summary(),
-            "gpu_launches": args.steps * launches_per_step, "e2e_matches_device_result": bool(same)}
+            "gpu_launches": args.steps * launches_per_step,
+            "e2e_matches_device_result": None if orient else bool(same)}
+    if orient:
+        line["p2p_assembled_sinogram_matches_single_launch"] = bool(same)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl)
     if tex is not None:
@@ -440,6 +475,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sampler", type=int, default=int(os.environ.get("TT_BENCH_SAMPLER", "1")), choices=[0, 1])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dev-one-gpu", action="store_true",
+                    help="validation only: every rank on cuda:0 with gloo (exercises the multi-rank data path, "
+                         "incl. the P2P shard writes, on a 1-GPU box; numbers are not a scaling measurement)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_env()

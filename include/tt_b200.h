@@ -246,6 +246,11 @@ typedef struct tt_trace_desc {
     int64_t img_stride; /* elements between images (0: n*n) */
     const float* wsoa;  /* optional pass-2 weight layout of wtab (tt_weights_soa, 24n bytes,
                            16-B aligned); NULL: converted into stream-ordered scratch per call */
+    int32_t partner_row; /* paired launches: first out/med row of the partner angles relative to
+                            out/med (<= 0: a_count/2, i.e. rows [cnt] + [cnt]).  An orientation
+                            shard writing straight into the full [A][F][n] sinogram passes
+                            out + a0 rows and partner_row = A/2 (batch 1). */
+    int32_t _pad3;
 } tt_trace_desc;
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
 
@@ -254,6 +259,20 @@ tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
  * w5im) -- 24n bytes at d_wsoa.  Pass the result as tt_trace_desc.wsoa to
  * reuse it across launches. */
 tt_status tt_weights_soa(const float* d_wtab, int n, float* d_wsoa, void* stream);
+
+/* Inter-process device pointers (CUDA IPC; over NVLink / NVSwitch between the
+ * GPUs of one node, or between processes on one GPU).  The multi-GPU driver
+ * hands rank 0's sinogram buffers to every rank, whose fused kernel then
+ * writes its orientation shard's rows straight into them (the gather is the
+ * kernel's own stores).  Export works for any pointer inside
+ * a cudaMalloc allocation (the handle carries the offset). */
+typedef struct tt_ipc_handle {
+    uint8_t bytes[64];
+    uint64_t offset;
+} tt_ipc_handle;
+tt_status tt_ipc_export(const void* d_ptr, tt_ipc_handle* out);
+tt_status tt_ipc_import(const tt_ipc_handle* h, int device, void** d_ptr);
+tt_status tt_ipc_close(void* d_ptr);
 
 /* P-functionals (circus features) of `rows` sinogram rows of
  * length n on device: circ[row][3] = (total variation, value at the weighted

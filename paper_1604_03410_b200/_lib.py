@@ -56,7 +56,12 @@ class TraceDesc(C.Structure):
     _fields_ = [("img", C.c_void_p), ("n", C.c_int32), ("a0", C.c_int32), ("a_count", C.c_int32),
                 ("full", C.c_int32), ("ctab", C.c_void_p), ("stab", C.c_void_p), ("wtab", C.c_void_p),
                 ("out", C.c_void_p), ("med", C.c_void_p), ("sampler", C.c_int32), ("pair_stride", C.c_int32),
-                ("batch", C.c_int32), ("_pad2", C.c_int32), ("img_stride", C.c_int64), ("wsoa", C.c_void_p)]
+                ("batch", C.c_int32), ("_pad2", C.c_int32), ("img_stride", C.c_int64), ("wsoa", C.c_void_p),
+                ("partner_row", C.c_int32), ("_pad3", C.c_int32)]
+
+
+class IpcHandle(C.Structure):
+    _fields_ = [("bytes", C.c_uint8 * 64), ("offset", C.c_uint64)]
 
 
 ARG_I32, ARG_I64, ARG_F32, ARG_F64, ARG_PTR = range(5)
@@ -99,6 +104,9 @@ _sigs = {
     "tt_ffma_probe": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "tt_trace_device": (_S, [C.POINTER(TraceDesc), C.c_void_p]),
     "tt_weights_soa": (_S, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    "tt_ipc_export": (_S, [C.c_void_p, C.POINTER(IpcHandle)]),
+    "tt_ipc_import": (_S, [C.POINTER(IpcHandle), C.c_int, C.POINTER(C.c_void_p)]),
+    "tt_ipc_close": (_S, [C.c_void_p]),
     "tt_circus_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_image_tex_create": (_S, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     "tt_image_atlas_create": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p)]),

@@ -30,6 +30,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cudaTypedefs.h>
+#include <mutex>
+
 #include "tt_b200.h"
 #include "tt_kernels.cuh"
 
@@ -1102,6 +1105,8 @@ static tt_status check_desc(const tt_trace_desc* d) {
     if (d->a_count < 0 || d->a0 < 0) return fail(nullptr, TT_ERR_INVALID, "negative angle range");
     if (d->pair_stride > 0 && d->a_count % 2 != 0)
         return fail(nullptr, TT_ERR_INVALID, "explicit pair_stride needs an even a_count");
+    if (d->partner_row > 0 && d->batch > 1)
+        return fail(nullptr, TT_ERR_INVALID, "partner_row applies to single-image launches");
     if ((long long)d->a_count * d->n >= (1ll << 31)) return fail(nullptr, TT_ERR_INVALID, "launch too large");
     if (d->batch < 0 || d->img_stride < 0) return fail(nullptr, TT_ERR_INVALID, "negative batch or stride");
     if (d->img_stride != 0 && d->img_stride < (long long)d->n * d->n)
@@ -1131,6 +1136,7 @@ static tt::TraceArgs to_args(const tt_trace_desc* d) {
     ta.stab = d->stab;
     ta.wtab = d->wtab;
     ta.wsoa = d->wsoa;
+    if (d->partner_row > 0 && ta.pair_stride > 0) ta.partner_row = d->partner_row;
     ta.out = d->out;
     ta.med = d->med;
     ta.full = d->full != 0;
@@ -1542,6 +1548,68 @@ tt_status tt_plan_chunks(const tt_plan* p, int* chunks) {
 tt_status tt_plan_destroy(tt_plan* p) {
     plan_release(p);
     return TT_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------- IPC
+
+namespace {
+std::mutex g_ipc_mu;
+std::map<void*, void*> g_ipc_open;  // imported pointer (base + offset) -> mapped base
+}  // namespace
+
+extern "C" {
+
+tt_status tt_ipc_export(const void* d_ptr, tt_ipc_handle* out) {
+    if (!d_ptr || !out) return fail(nullptr, TT_ERR_INVALID, "null argument");
+    static PFN_cuMemGetAddressRange_v3020 range = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(f);
+    }();
+    if (!range) return fail(nullptr, TT_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, CUdeviceptr(d_ptr)) != CUDA_SUCCESS)
+        return fail(nullptr, TT_ERR_INVALID, "pointer is not inside a device allocation");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == sizeof(out->bytes), "IPC handle size");
+    std::memcpy(out->bytes, &h, sizeof(h));
+    out->offset = std::uint64_t(CUdeviceptr(d_ptr) - base);
+    return TT_OK;
+}
+
+tt_status tt_ipc_import(const tt_ipc_handle* hd, int device, void** d_ptr) {
+    if (!hd || !d_ptr) return fail(nullptr, TT_ERR_INVALID, "null argument");
+    DeviceGuard guard(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hd->bytes, sizeof(h));
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaIpcOpenMemHandle");
+    *d_ptr = static_cast<char*>(base) + hd->offset;
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    g_ipc_open[*d_ptr] = base;
+    return TT_OK;
+}
+
+tt_status tt_ipc_close(void* d_ptr) {
+    void* base = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_ipc_mu);
+        auto it = g_ipc_open.find(d_ptr);
+        if (it == g_ipc_open.end()) return fail(nullptr, TT_ERR_INVALID, "pointer was not imported");
+        base = it->second;
+        g_ipc_open.erase(it);
+    }
+    cudaError_t e = cudaIpcCloseMemHandle(base);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "cudaIpcCloseMemHandle");
 }
 
 }  // extern "C"

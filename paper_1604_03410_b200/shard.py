@@ -66,3 +66,33 @@ def image_shard(images: int, world: int, rank: int):
     """Contiguous block of image indices for rank (batched feature extraction)."""
     lo = rank * images // world
     return lo, (rank + 1) * images // world - lo
+
+
+def direct_shard_rows(angles: int, world: int, rank: int, F: int, n: int):
+    """Launch geometry of rank's orientation shard written straight into the
+    full [angles][F][n] sinogram (and [angles][2][n] medians): returns
+    (a0, a_count, pair_stride, row0, partner_row) for tt_trace_device with
+    out = base + row0 rows and partner_row = angles / 2."""
+    a0, cnt, h = orientation_shard(angles, world, rank)
+    return a0, 2 * cnt, h, a0, h
+
+
+def share_device_buffers(ptrs, dist, device: int, src: int = 0, group=None):
+    """Rank `src` exports its device pointers (CUDA IPC handles), every rank
+    maps them (peer access over NVLink / NVSwitch).  Returns (pointers,
+    close) where close() unmaps the imported ones.  The fused kernel then
+    writes each shard's rows directly into rank src's buffers: the sinogram
+    assembly needs no gather collective, only a completion signal."""
+    from . import trace as _tr
+
+    rank = dist.get_rank(group)
+    handles = [[_tr.ipc_export(p) for p in ptrs] if rank == src else None]
+    dist.broadcast_object_list(handles, src=src, group=group)
+    if rank == src:
+        return list(ptrs), (lambda: None)
+    mapped = [_tr.ipc_import(h, device) for h in handles[0]]
+
+    def close():
+        for p in mapped:
+            _tr.ipc_close(p)
+    return mapped, close

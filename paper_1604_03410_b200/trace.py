@@ -222,15 +222,35 @@ class Plan:
 
 def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, stab_ptr: int, wtab_ptr: int,
                  out_ptr: int, med_ptr: int = 0, full: bool = True, sampler: int = 0, stream: int = 0,
-                 tex=None, pair_stride: int = 0, batch: int = 1, img_stride: int = 0, wsoa_ptr: int = 0) -> None:
+                 tex=None, pair_stride: int = 0, batch: int = 1, img_stride: int = 0, wsoa_ptr: int = 0,
+                 partner_row: int = 0) -> None:
     """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex); pair_stride, batch, wsoa as in
     tt_b200.h (wsoa_ptr: a prepared weights_soa() buffer; 0 converts wtab per call)."""
     d = _lib.TraceDesc(img_ptr, n, a0, a_count, int(full), ctab_ptr, stab_ptr, wtab_ptr or None, out_ptr,
-                       med_ptr or None, sampler, pair_stride, batch, 0, img_stride, wsoa_ptr or None)
+                       med_ptr or None, sampler, pair_stride, batch, 0, img_stride, wsoa_ptr or None, partner_row, 0)
     if tex is not None:
         _check(lib.tt_trace_device_tex(C.byref(d), tex, C.c_void_p(stream)))
     else:
         _check(lib.tt_trace_device(C.byref(d), C.c_void_p(stream)))
+
+
+def ipc_export(ptr: int) -> bytes:
+    """Inter-process handle (72 bytes) of a device pointer inside a cudaMalloc allocation."""
+    h = _lib.IpcHandle()
+    _check(lib.tt_ipc_export(C.c_void_p(ptr), C.byref(h)))
+    return bytes(h)
+
+
+def ipc_import(handle: bytes, device: int) -> int:
+    """Map another process's exported device pointer into this one (peer access over NVLink)."""
+    h = _lib.IpcHandle.from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(lib.tt_ipc_import(C.byref(h), device, C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib.tt_ipc_close(C.c_void_p(ptr)))
 
 
 def weights_soa(wtab_ptr: int, n: int, wsoa_ptr: int, stream: int = 0) -> None:
