@@ -252,7 +252,8 @@ def run_ours(args, ws, rank, local):
             image_texture_update(tex, img.data_ptr(), 0, sptr)
         tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
                         out_ptr, med_ptr, full=full, sampler=args.sampler, stream=sptr, tex=tex,
-                        pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0, partner_row=prow)
+                        pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0, partner_row=prow,
+                        peer_out=orient and rank != 0)
 
     def features():
         if feats_on:  # P-functional (circus) stage consuming the sinograms

@@ -250,8 +250,10 @@ typedef struct tt_trace_desc {
                             out/med (<= 0: a_count/2, i.e. rows [cnt] + [cnt]).  An orientation
                             shard writing straight into the full [A][F][n] sinogram passes
                             out + a0 rows and partner_row = A/2 (batch 1). */
-    int32_t _pad3;
+    int32_t flags;       /* TT_TRACE_PEER_OUT: out/med are another GPU's memory (IPC / NVLink):
+                            each thread fences its stores at system scope before it exits */
 } tt_trace_desc;
+#define TT_TRACE_PEER_OUT 1
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
 
 /* Regroup a [n][8] weight table (tt_make_tables) on device into the fused

@@ -1137,6 +1137,7 @@ static tt::TraceArgs to_args(const tt_trace_desc* d) {
     ta.wtab = d->wtab;
     ta.wsoa = d->wsoa;
     if (d->partner_row > 0 && ta.pair_stride > 0) ta.partner_row = d->partner_row;
+    ta.peer_out = (d->flags & TT_TRACE_PEER_OUT) != 0;
     ta.out = d->out;
     ta.med = d->med;
     ta.full = d->full != 0;

@@ -30,6 +30,7 @@ struct TraceArgs {
     int a_count = 0;              // launch units (angles a0 .. a0+a_count-1)
     int pair_stride = 0;          // >0: unit i also owns angle a0+i+pair_stride (rows partner_row+i)
     int partner_row = -1;         // first output row of the partner angles (-1: a_count; batch == 1 only)
+    bool peer_out = false;        // out/med live in another GPU's memory: system-scope fence before exit
     const float* ctab = nullptr;  // [A_total] cos(theta_a), f64 -> f32 on host
     const float* stab = nullptr;  // [A_total] sin(theta_a)
     const float* wtab = nullptr;  // [n][8]: r, r^2, w3re, w3im, w4re, w4im, w5re, w5im (spec §2.2), 16-B aligned

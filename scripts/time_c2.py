@@ -25,7 +25,8 @@ flush = torch.empty(64 << 20, device="cuda")
 stream = torch.cuda.Stream()
 sp = stream.cuda_stream
 tt.weights_soa(wt.data_ptr(), n, wsoa.data_ptr(), sp)
-tex = image_texture(img.data_ptr(), n, sp)
+sampler = int(os.environ.get("TT_SAMPLER_ID", "1"))  # 1 texture gather, 0 LDG
+tex = image_texture(img.data_ptr(), n, sp) if sampler == 1 else None
 ts = []
 for i in range(reps + 3):
     with torch.cuda.stream(stream):
@@ -33,11 +34,12 @@ for i in range(reps + 3):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
-                    med.data_ptr() if full else 0, full=full, stream=sp, tex=tex, wsoa_ptr=wsoa.data_ptr())
+                    med.data_ptr() if full else 0, full=full, sampler=sampler, stream=sp, tex=tex,
+                    wsoa_ptr=wsoa.data_ptr())
     e1.record(stream)
     e1.synchronize()
     if i >= 3:
         ts.append(e0.elapsed_time(e1))
 ts.sort()
-print(json.dumps({"lib": os.environ.get("TT_LIB_PATH", "default"), "n": n, "A": A, "full": full,
+print(json.dumps({"lib": os.environ.get("TT_LIB_PATH", "default"), "n": n, "A": A, "full": full, "sampler": sampler,
                   "median_ms": ts[len(ts) // 2], "min_ms": ts[0], "checksum": float(out.double().sum())}))

@@ -38,7 +38,8 @@ def _worker(rank, world, port, n, A, result):
     ptrs, close = shard.share_device_buffers([out.data_ptr(), med.data_ptr()] if rank == 0 else [], dist, 0)
     a0, cnt, pair, row0, prow = shard.direct_shard_rows(A, world, rank, F, n)
     tt.trace_device(img.data_ptr(), n, a0, cnt, ct.data_ptr(), st.data_ptr(), wt.data_ptr(),
-                    ptrs[0] + row0 * F * n * 4, ptrs[1] + row0 * 2 * n * 4, pair_stride=pair, partner_row=prow)
+                    ptrs[0] + row0 * F * n * 4, ptrs[1] + row0 * 2 * n * 4, pair_stride=pair, partner_row=prow,
+                    peer_out=rank != 0)
     torch.cuda.synchronize()
     dist.barrier()  # every shard's rows are in rank 0's buffers
     if rank == 0:
