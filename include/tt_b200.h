@@ -214,6 +214,22 @@ int tt_max_full_n(void);
  * count behind the FLOP roofline). */
 uint64_t tt_count_inbounds_taps(int n, int a0, int a_count, const float* ctab, const float* stab);
 
+/* ---- input formats (the caller side of the path) ------------------------------
+ * A photograph is h x w pixels of 1 (gray) or 3 (RGB) 8-bit channels; the
+ * transform wants an n x n f32 image whose inscribed disk holds the whole
+ * picture, so no rotation loses mass.  tt_prep_side gives that n (the smallest
+ * n with (n-1)^2 >= h^2 + w^2, i.e. the picture's diagonal fits the disk of
+ * radius (n-1)/2 around the centre o); tt_prep_device converts and pads on the
+ * GPU: gray = ((0.299 r + 0.587 g) + 0.114 b) / 255 in f32 (RGB) or v / 255
+ * (gray), placed with its top-left corner at ((n-w)/2, (n-h)/2), zeros
+ * elsewhere.  The PNM reader/writer handle binary P5 (gray) / P6 (RGB) 8-bit
+ * files. */
+int tt_prep_side(int h, int w);
+tt_status tt_prep_device(const uint8_t* d_pix, int h, int w, int channels, int n, float* d_img, void* stream);
+/* *h = *w = *channels = 0 on entry returns the header only (pix may be NULL). */
+tt_status tt_pnm_read(const char* path, int* h, int* w, int* channels, uint8_t* pix, size_t cap);
+tt_status tt_pgm_write(const char* path, const float* img, int h, int w, float lo, float hi);
+
 /* FP32 roofline probe: enqueue blocks x 256 threads x iters x 128 FFMA on
  * `stream` (2 flop each); out needs `blocks` floats of device memory. */
 tt_status tt_ffma_probe(float* d_out, int blocks, int iters, void* stream);

@@ -185,3 +185,23 @@ def tier2(img, n, ctab, stab, wtab, *, a0=0, a_count=None, threads=1, lines=0):
     out = raw[:nout].view(np.float32).reshape(a_count, 6, n)
     med = raw[nout:].view(np.int32).reshape(a_count, 2, n)
     return out, med, rep
+
+
+def prep(pix, n: int):
+    """CPU restatement of tt_prep_device (tt_b200.h; caller-side input format):
+    8-bit gray [h][w] or RGB [h][w][3] -> n x n f32 gray placed at
+    ((n-w)//2, (n-h)//2), zeros elsewhere; gray = ((0.299 r + 0.587 g) + 0.114 b) / 255
+    in IEEE f32 (numpy float32 arithmetic never contracts)."""
+    pix = np.asarray(pix, np.uint8)
+    h, w = pix.shape[:2]
+    f = pix.astype(np.float32)
+    if pix.ndim == 3:
+        r, g, b = f[..., 0], f[..., 1], f[..., 2]
+        v = (np.float32(0.299) * r + np.float32(0.587) * g) + np.float32(0.114) * b
+    else:
+        v = f
+    v = (v / np.float32(255.0)).astype(np.float32)
+    out = np.zeros((n, n), np.float32)
+    y0, x0 = (n - h) // 2, (n - w) // 2
+    out[y0:y0 + h, x0:x0 + w] = v
+    return out

@@ -22,5 +22,5 @@ from .api import (  # noqa: F401
 )
 from .trace import (  # noqa: F401
     CIRCUS, DISK, PHANTOM, SEEDS, SPARSE, Plan, TRACE_T05, TRACE_T05_BATCH, RADON, TraceTransform, circus, circus_device, make_tables,
-    ipc_close, ipc_export, ipc_import, max_full_n, schedule_slots, synth_image, trace_device, weights_soa,
+    ipc_close, ipc_export, ipc_import, max_full_n, prep_device, prep_side, read_pnm, write_pgm, schedule_slots, synth_image, trace_device, weights_soa,
 )

@@ -101,6 +101,11 @@ _sigs = {
     "tt_schedule_slots": (C.c_int, [C.c_int, C.c_int]),
     "tt_max_full_n": (C.c_int, []),
     "tt_count_inbounds_taps": (C.c_uint64, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "tt_prep_side": (C.c_int, [C.c_int, C.c_int]),
+    "tt_prep_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "tt_pnm_read": (_S, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p,
+                         C.c_size_t]),
+    "tt_pgm_write": (_S, [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_float]),
     "tt_ffma_probe": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "tt_trace_device": (_S, [C.POINTER(TraceDesc), C.c_void_p]),
     "tt_weights_soa": (_S, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),

@@ -1,17 +1,24 @@
 // tt_host.cpp — host-side inputs of the trace transform (product side):
-// angle/weight tables and the deterministic synthetic images of DESIGN.md
-// §2.1-2.4.  These are inputs the caller hands to the device kernels (the
+// angle/weight tables, the deterministic synthetic images of DESIGN.md
+// §2.1-2.4, and the picture formats on the caller side (PNM files, the
+// grayscale + circumscribed-square preparation launcher).  These are inputs the caller hands to the device kernels (the
 // reference-style DSL kernel takes ctab/stab as array arguments, SURVEY.md
 // Appendix B); the independent restatement in oracle/tt_oracle.c checks them
 // bit-for-bit (tests/test_host_inputs.py).
 //
 // Compiled with -ffp-contract=off (like /root/reference/proj/CMakeLists.txt:15-16)
 // so every f64 expression rounds exactly as written.
+#include <algorithm>
 #include <cmath>
-#include <cstdint>
 #include <cstddef>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#include <cuda_runtime.h>
 
 #include "tt_b200.h"
+#include "tt_kernels.cuh"
 
 namespace {
 
@@ -176,4 +183,87 @@ extern "C" std::uint64_t tt_count_inbounds_taps(int n, int a0, int a_count, cons
         }
     }
     return total;
+}
+
+// ---------------------------------------------------------------- formats
+
+extern "C" int tt_prep_side(int h, int w) {
+    if (h < 1 || w < 1) return 0;
+    const std::uint64_t d2 = std::uint64_t(h) * h + std::uint64_t(w) * w;
+    std::uint64_t m = std::uint64_t(std::sqrt(double(d2)));
+    while (m * m < d2) ++m;  // m = ceil(sqrt(h^2 + w^2)) exactly
+    while (m > 0 && (m - 1) * (m - 1) >= d2) --m;
+    return int(m + 1);
+}
+
+extern "C" tt_status tt_prep_device(const std::uint8_t* d_pix, int h, int w, int channels, int n, float* d_img,
+                                   void* stream) {
+    if (!d_pix || !d_img || h < 1 || w < 1 || (channels != 1 && channels != 3) || n < std::max(h, w))
+        return TT_ERR_INVALID;
+    cudaError_t e = tt::launch_prep(d_pix, h, w, channels, n, d_img, (cudaStream_t)stream);
+    return e == cudaSuccess ? TT_OK : TT_ERR_CUDA;
+}
+
+namespace {
+int pnm_token(std::FILE* f) {  // next decimal header field, skipping whitespace and # comments
+    int c = std::fgetc(f);
+    for (;;) {
+        while (c == ' ' || c == '\t' || c == '\r' || c == '\n') c = std::fgetc(f);
+        if (c != '#') break;
+        while (c != '\n' && c != EOF) c = std::fgetc(f);
+    }
+    if (c < '0' || c > '9') return -1;
+    long v = 0;
+    while (c >= '0' && c <= '9') {
+        v = v * 10 + (c - '0');
+        if (v > (1 << 28)) return -1;
+        c = std::fgetc(f);
+    }
+    return int(v);  // the single whitespace after maxval is consumed here
+}
+}  // namespace
+
+extern "C" tt_status tt_pnm_read(const char* path, int* h, int* w, int* channels, std::uint8_t* pix, std::size_t cap) {
+    if (!path || !h || !w || !channels) return TT_ERR_INVALID;
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) return TT_ERR_INVALID;
+    char m[2] = {0, 0};
+    tt_status st = TT_ERR_INVALID;
+    if (std::fread(m, 1, 2, f) == 2 && m[0] == 'P' && (m[1] == '5' || m[1] == '6')) {
+        const int ww = pnm_token(f), hh = pnm_token(f), mx = pnm_token(f);
+        const int ch = m[1] == '6' ? 3 : 1;
+        if (ww > 0 && hh > 0 && mx == 255) {
+            const std::size_t bytes = std::size_t(ww) * hh * ch;
+            if (!pix) {
+                st = TT_OK;
+            } else if (cap >= bytes && std::fread(pix, 1, bytes, f) == bytes) {
+                st = TT_OK;
+            }
+            if (st == TT_OK) {
+                *h = hh;
+                *w = ww;
+                *channels = ch;
+            }
+        }
+    }
+    std::fclose(f);
+    return st;
+}
+
+extern "C" tt_status tt_pgm_write(const char* path, const float* img, int h, int w, float lo, float hi) {
+    if (!path || !img || h < 1 || w < 1 || !(hi > lo)) return TT_ERR_INVALID;
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) return TT_ERR_INVALID;
+    std::fprintf(f, "P5\n%d %d\n255\n", w, h);
+    std::vector<std::uint8_t> row(static_cast<std::size_t>(w));
+    for (int y = 0; y < h; ++y) {
+        for (int x = 0; x < w; ++x) {
+            const double t = (double(img[std::size_t(y) * w + x]) - lo) / (double(hi) - lo);
+            row[x] = std::uint8_t(std::lround(std::min(1.0, std::max(0.0, t)) * 255.0));
+        }
+        std::fwrite(row.data(), 1, row.size(), f);
+    }
+    const bool ok = std::fflush(f) == 0;
+    std::fclose(f);
+    return ok ? TT_OK : TT_ERR_INVALID;
 }

@@ -115,6 +115,9 @@ cudaError_t make_image_atlas(const float* imgs, int n, int batch, long long stri
 cudaError_t fill_image_atlas(cudaArray_t arr, const float* imgs, int n, int batch, long long stride, int cols,
                              cudaStream_t s, int b0 = 0);
 
+// 8-bit gray/RGB picture (h x w x ch) -> n x n f32 gray, centred, zero padded.
+cudaError_t launch_prep(const uint8_t* pix, int h, int w, int ch, int n, float* img, cudaStream_t s);
+
 // Writes a buffer larger than L2 (timing hygiene between bench iterations).
 cudaError_t launch_l2_flush(void* buf, uint64_t bytes, cudaStream_t s);
 

@@ -234,6 +234,36 @@ def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, sta
         _check(lib.tt_trace_device(C.byref(d), C.c_void_p(stream)))
 
 
+def prep_side(h: int, w: int) -> int:
+    """Side n of the square whose inscribed disk holds an h x w picture (tt_prep_side)."""
+    return lib.tt_prep_side(h, w)
+
+
+def read_pnm(path: str) -> np.ndarray:
+    """Binary P5/P6 8-bit image -> uint8 [h][w] or [h][w][3] (tt_pnm_read)."""
+    h, w, c = C.c_int(0), C.c_int(0), C.c_int(0)
+    _check(lib.tt_pnm_read(path.encode(), C.byref(h), C.byref(w), C.byref(c), None, 0))
+    pix = np.empty((h.value, w.value, c.value), np.uint8)
+    _check(lib.tt_pnm_read(path.encode(), C.byref(h), C.byref(w), C.byref(c), C.c_void_p(pix.ctypes.data),
+                           pix.nbytes))
+    return pix[..., 0] if c.value == 1 else pix
+
+
+def write_pgm(path: str, img: np.ndarray, lo: float | None = None, hi: float | None = None) -> None:
+    """f32 image -> 8-bit P5 file, linearly mapping [lo, hi] (default: min..max) to 0..255."""
+    img = np.ascontiguousarray(img, np.float32)
+    lo = float(img.min()) if lo is None else lo
+    hi = float(img.max()) if hi is None else hi
+    if hi <= lo:
+        hi = lo + 1.0
+    _check(lib.tt_pgm_write(path.encode(), C.c_void_p(img.ctypes.data), img.shape[0], img.shape[1], lo, hi))
+
+
+def prep_device(pix_ptr: int, h: int, w: int, channels: int, n: int, img_ptr: int, stream: int = 0) -> None:
+    """8-bit picture on device -> n x n f32 gray, centred, zero padded (tt_prep_device)."""
+    _check(lib.tt_prep_device(C.c_void_p(pix_ptr), h, w, channels, n, C.c_void_p(img_ptr), C.c_void_p(stream)))
+
+
 def ipc_export(ptr: int) -> bytes:
     """Inter-process handle (72 bytes) of a device pointer inside a cudaMalloc allocation."""
     h = _lib.IpcHandle()
