@@ -310,6 +310,11 @@ tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, int64_t img_
 tt_status tt_image_tex_destroy(tt_image_tex* t);
 tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, void* stream);
 
+/* VPTX JIT (kernels without a native implementation are compiled from their
+ * VPTX bodies at tt_get_function: VPTX -> CUDA C++ -> NVRTC -> sm_100a).  This
+ * returns the generated CUDA C++ for `kernel` without compiling (diagnostics). */
+tt_status tt_jit_source(const char* vptx, size_t len, const char* kernel, char* buf, size_t cap, size_t* needed);
+
 /* ---- plans: the host-to-host form of the path -------------------------------
  * One plan = one (n, angles, functionals, batch) configuration with its device
  * tables, image texture and output buffers resident.  tt_plan_run uploads the

@@ -15,8 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtt_b200.so")
 
-SOURCES = ["tt_kernels.cu", "tt_context.cpp", "tt_host.cpp"]
-HEADERS = ["tt_kernels.cuh"]
+SOURCES = ["tt_kernels.cu", "tt_context.cpp", "tt_host.cpp", "tt_jit.cpp"]
+HEADERS = ["tt_kernels.cuh", "tt_jit.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         return LIB
     cmd = ["nvcc", "-ccbin", "g++", "-shared", "-Xcompiler", "-fPIC,-ffp-contract=off", *ARCH, "-O3",
            "-lineinfo", "-std=c++17", "-I" + os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines],
-           *[os.path.join(CSRC, f) for f in SOURCES], "-o", target + ".tmp"]
+           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl", "-o", target + ".tmp"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

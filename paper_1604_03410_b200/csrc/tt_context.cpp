@@ -16,6 +16,7 @@
 // The emulated execution engine (emulator.hpp run_kernel) is replaced by the
 // sm_100a kernels in tt_kernels.cu; nothing here computes on the CPU.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cctype>
 #include <climits>
@@ -34,6 +35,7 @@
 #include <mutex>
 
 #include "tt_b200.h"
+#include "tt_jit.h"
 #include "tt_kernels.cuh"
 
 namespace {
@@ -68,6 +70,7 @@ struct Param {
 struct KernelDecl {
     std::string name;
     std::vector<Param> params;
+    std::vector<tt::jit::Line> body;  // instructions / declarations between '{' and '}' (JIT input)
     std::string signature() const {  // Signature::to_string, types.hpp:104-111
         std::string s = name + "(";
         for (std::size_t i = 0; i < params.size(); ++i) {
@@ -98,6 +101,10 @@ using LaunchFn = LaunchOutcome (*)(tt_ctx&, const tt_grid&, const std::vector<Re
 struct NativeKernel {
     KernelDecl decl;
     LaunchFn fn;
+    // The fused trace kernels stand in for their documented DSL bodies (oracle/trace_t05.krn,
+    // bit-exact vs the reference engine) whatever body a module carries; the sample kernels only
+    // bind to header-only modules -- a module with a real VPTX body runs that body (JIT).
+    bool replaces_body = false;
 };
 
 const std::vector<NativeKernel>& registry();
@@ -142,10 +149,18 @@ struct Module {
     std::vector<KernelDecl> kernels;
 };
 
+// A kernel without a native implementation, compiled from its VPTX body (tt_jit.h).
+struct JitFunction {
+    KernelDecl decl;
+    tt::jit::Program prog;
+    ~JitFunction() { tt::jit::release(prog); }
+};
+
 struct FunctionEntry {
     std::uint64_t module_id = 0;
     std::string kernel;
     const NativeKernel* native = nullptr;
+    std::shared_ptr<JitFunction> jit;  // set when native == nullptr
 };
 
 std::atomic<std::uint64_t> g_next_ctx_id{0};
@@ -176,6 +191,10 @@ struct tt_ctx {
     std::string last_error;
     std::map<std::uint64_t, TexEntry> tex_cache;      // keyed by image allocation base
     std::map<std::uint64_t, WeightEntry> w_cache;     // keyed by wtab allocation base
+    // JIT launches: the device trap record and the allocation table the bounds checks search
+    tt::jit::TrapRecord* jit_trap = nullptr;
+    unsigned long long* jit_rng = nullptr;
+    std::size_t jit_rng_cap = 0;  // entries (3 words each)
 };
 
 namespace {
@@ -367,6 +386,7 @@ tt_status parse_module(tt_ctx* ctx, const char* text, std::size_t len, Module& m
                 closed = true;
                 break;
             }
+            kd.body.push_back(tt::jit::Line{b.no, b.toks});
         }
         if (!closed) return syntax(lines.back().no, "unterminated kernel body");
         for (const auto& other : m.kernels)
@@ -632,6 +652,8 @@ const std::vector<NativeKernel>& registry() {
             nk.decl.name = name;
             nk.decl.params = std::move(ps);
             nk.fn = fn;
+            const std::string nm = name;
+            nk.replaces_body = nm == "trace_t05" || nm == "trace_t05_batch" || nm == "radon" || nm == "circus";
             r.push_back(std::move(nk));
         };
         const Scalar f = Scalar::F32, d = Scalar::F64, i = Scalar::I32, l = Scalar::I64;
@@ -747,6 +769,10 @@ tt_status tt_ctx_destroy(tt_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     while (!ctx->tex_cache.empty()) drop_texture(ctx, ctx->tex_cache.begin()->first);
     while (!ctx->w_cache.empty()) drop_weights(ctx, ctx->w_cache.begin()->first);
+    if (ctx->jit_trap) cudaFree(ctx->jit_trap);
+    if (ctx->jit_rng) cudaFree(ctx->jit_rng);
+    ctx->jit_trap = nullptr;
+    ctx->jit_rng = nullptr;
     for (auto& kv : ctx->allocs)
         if (kv.second.live && kv.second.dptr) cudaFreeAsync(kv.second.dptr, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
@@ -837,13 +863,31 @@ tt_status tt_get_function(tt_ctx* ctx, tt_module m, const char* name, tt_functio
     for (const auto& k : it->second.kernels)
         if (k.name == name) decl = &k;
     if (!decl) return fail(ctx, TT_ERR_FUNCTION_NOT_FOUND, std::string("FunctionNotFound: '") + name + "'");
+    // header-only module (no body, or a bare `ret` as the C ABI's own renderers emit)
+    const bool header_only =
+        decl->body.empty() || (decl->body.size() == 1 && decl->body[0].toks.size() == 1 && decl->body[0].toks[0] == "ret");
     const NativeKernel* nk = find_native(*decl);
-    if (!nk)
-        return fail(ctx, TT_ERR_FUNCTION_NOT_FOUND,
-                    std::string("FunctionNotFound: '") + name + "' (no native sm_100a kernel for " +
-                        decl->signature() + "; see tt_native_kernels)");
+    if (nk && !header_only && !nk->replaces_body) nk = nullptr;  // run the module's own body
+    std::shared_ptr<JitFunction> jf;
+    if (!nk) {
+        if (header_only)
+            return fail(ctx, TT_ERR_FUNCTION_NOT_FOUND,
+                        std::string("FunctionNotFound: '") + name + "' (no native sm_100a kernel for " +
+                            decl->signature() + " and no VPTX body to compile; see tt_native_kernels)");
+        // No native implementation: compile the VPTX body for sm_100a (tt_jit.h).
+        DeviceGuard guard(ctx->device);
+        jf = std::make_shared<JitFunction>();
+        jf->decl = *decl;
+        std::vector<tt::jit::Param> jp;
+        for (const Param& p : decl->params)
+            jp.push_back(tt::jit::Param{p.ptr, tt::jit::Ty(static_cast<int>(p.type)), p.name});
+        std::string err;
+        if (!tt::jit::compile(decl->name, jp, decl->body, jf->prog, err))
+            return fail(ctx, err.rfind("VPTX JIT, line", 0) == 0 ? TT_ERR_VALIDATION_FAILED : TT_ERR_CUDA,
+                        (err.rfind("VPTX JIT, line", 0) == 0 ? "ValidationFailed:\n  " : "") + err);
+    }
     const std::uint64_t h = ctx->next_handle++;
-    ctx->functions.emplace(h, FunctionEntry{m.id, name, nk});
+    ctx->functions.emplace(h, FunctionEntry{m.id, name, nk, jf});
     ++ctx->c.functions_resolved;
     ctx->events.push_back(TT_EV_FUNCTION_RESOLVE);
     *out = tt_function{ctx->id, h};
@@ -954,6 +998,105 @@ tt_status tt_host_free(void* p) {
 
 // ---- launch ---------------------------------------------------------------
 
+}  // extern "C"
+
+namespace {
+
+// Launch of a JIT-compiled VPTX kernel: the context's allocation table goes to
+// the device for the bounds checks, the trap record is reset, and after the
+// launch the first trap (emulator order, tt_jit.h) is read back.
+LaunchOutcome run_jit(tt_ctx& ctx, JitFunction& jf, const tt_grid& g, const std::vector<ResolvedArg>& a,
+                      std::uint64_t shared_total) {
+    LaunchOutcome o;
+    auto cuda_err = [&](cudaError_t e, const char* what) {
+        o.status = TT_ERR_CUDA;
+        o.error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+        return o;
+    };
+    // allocation table: live ranges, then freed ranges that overlap nothing already listed
+    std::vector<std::array<unsigned long long, 3>> rng;
+    for (int pass = 0; pass < 2; ++pass)
+        for (const auto& kv : ctx.allocs) {
+            const Alloc& al = kv.second;
+            if (al.live != (pass == 0) || !al.dptr) continue;
+            const unsigned long long b = (unsigned long long)al.dptr, e = b + al.bytes;
+            bool overlap = false;
+            if (pass == 1)
+                for (const auto& r : rng) overlap = overlap || (b < r[1] && r[0] < e) || b == r[0];
+            if (!overlap) rng.push_back({b, e, al.live ? 1ull : 0ull});
+        }
+    std::sort(rng.begin(), rng.end());
+    cudaError_t e = cudaSuccess;
+    if (!ctx.jit_trap && (e = cudaMalloc((void**)&ctx.jit_trap, sizeof(tt::jit::TrapRecord))) != cudaSuccess)
+        return cuda_err(e, "JIT trap record");
+    if (rng.size() > ctx.jit_rng_cap) {
+        if (ctx.jit_rng) cudaFree(ctx.jit_rng);
+        ctx.jit_rng_cap = std::max<std::size_t>(64, rng.size() * 2);
+        if ((e = cudaMalloc((void**)&ctx.jit_rng, ctx.jit_rng_cap * 24)) != cudaSuccess) {
+            ctx.jit_rng = nullptr;
+            ctx.jit_rng_cap = 0;
+            return cuda_err(e, "JIT allocation table");
+        }
+    }
+    tt::jit::TrapRecord rec0{};
+    rec0.key = ~0ull;
+    if (!rng.empty() && (e = cudaMemcpyAsync(ctx.jit_rng, rng.data(), rng.size() * 24, cudaMemcpyHostToDevice,
+                                            ctx.stream)) != cudaSuccess)
+        return cuda_err(e, "JIT allocation table upload");
+    if ((e = cudaMemcpyAsync(ctx.jit_trap, &rec0, sizeof rec0, cudaMemcpyHostToDevice, ctx.stream)) != cudaSuccess)
+        return cuda_err(e, "JIT trap reset");
+    // kernel arguments: the VPTX parameters (pointers as device addresses), then the hidden ones
+    std::vector<std::array<unsigned char, 8>> store(a.size() + 4);
+    std::vector<void*> argv;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        auto& cell = store[i];
+        if (a[i].kind == TT_ARG_PTR) {
+            const long long v = (long long)a[i].dptr;
+            std::memcpy(cell.data(), &v, 8);
+        } else if (a[i].kind == TT_ARG_I32) {
+            std::memcpy(cell.data(), &a[i].value.v.i32, 4);
+        } else if (a[i].kind == TT_ARG_I64) {
+            std::memcpy(cell.data(), &a[i].value.v.i64, 8);
+        } else if (a[i].kind == TT_ARG_F32) {
+            std::memcpy(cell.data(), &a[i].value.v.f32, 4);
+        } else {
+            std::memcpy(cell.data(), &a[i].value.v.f64, 8);
+        }
+        argv.push_back(cell.data());
+    }
+    void* trap_ptr = ctx.jit_trap;
+    const unsigned long long* rng_ptr = ctx.jit_rng;
+    int nr = int(rng.size());
+    unsigned shb = unsigned(shared_total);
+    argv.push_back(&trap_ptr);
+    argv.push_back(&rng_ptr);
+    argv.push_back(&nr);
+    argv.push_back(&shb);
+    e = cudaLaunchKernel((const void*)jf.prog.kernel, dim3(g.grid[0], g.grid[1], g.grid[2]),
+                         dim3(g.block[0], g.block[1], g.block[2]), argv.data(), shared_total, ctx.stream);
+    if (e != cudaSuccess) return cuda_err(e, "JIT kernel launch");
+    o.gpu_launches = 1;
+    tt::jit::TrapRecord rec{};
+    if ((e = cudaMemcpyAsync(&rec, ctx.jit_trap, sizeof rec, cudaMemcpyDeviceToHost, ctx.stream)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(ctx.stream)) != cudaSuccess)
+        return cuda_err(e, "JIT kernel");
+    if (rec.key != ~0ull) {
+        o.trap.trapped = 1;
+        o.trap.kind = rec.kind;
+        for (int i = 0; i < 3; ++i) {
+            o.trap.thread[i] = rec.tid[i] + 1;  // 1-indexed, source-language convention
+            o.trap.block[i] = rec.ctaid[i] + 1;
+        }
+        o.trap.instr_index = std::uint64_t(rec.instr);
+        o.trap.code = rec.kind == TT_TRAP_EXPLICIT ? rec.code : 0;
+    }
+    return o;
+}
+
+}  // namespace
+
+extern "C" {
+
 tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_arg* args, int nargs, tt_trap* trap_out) {
     TT_CHECK_CTX(ctx);
     if (!cfg || (nargs > 0 && !args) || nargs < 0) return fail(ctx, TT_ERR_INVALID, "null argument");
@@ -963,7 +1106,9 @@ tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_ar
         return fail(ctx, TT_ERR_FUNCTION_NOT_FOUND, "FunctionNotFound: 'stale or foreign function handle'");
     if (ctx->modules.find(fit->second.module_id) == ctx->modules.end())
         return fail(ctx, TT_ERR_FUNCTION_NOT_FOUND, "FunctionNotFound: 'function's module was unloaded'");
-    const NativeKernel& nk = *fit->second.native;
+    const NativeKernel* native = fit->second.native;
+    const std::shared_ptr<JitFunction> jit = fit->second.jit;
+    const KernelDecl& decl = native ? native->decl : jit->decl;
 
     // driver.hpp:229-231: convert every argument (ownership, liveness) first.
     std::vector<ResolvedArg> ra(static_cast<std::size_t>(nargs));
@@ -991,12 +1136,12 @@ tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_ar
         return fail(ctx, TT_ERR_LAUNCH_CONFIG, "LaunchConfigError: block of " + std::to_string(tpb) +
                                                    " threads exceeds the cap of " +
                                                    std::to_string(ctx->caps.max_block_threads));
-    if (std::size_t(nargs) != nk.decl.params.size())
-        return fail(ctx, TT_ERR_ARGUMENT_MISMATCH, "ArgumentMismatch: kernel '" + nk.decl.name + "' takes " +
-                                                       std::to_string(nk.decl.params.size()) +
+    if (std::size_t(nargs) != decl.params.size())
+        return fail(ctx, TT_ERR_ARGUMENT_MISMATCH, "ArgumentMismatch: kernel '" + decl.name + "' takes " +
+                                                       std::to_string(decl.params.size()) +
                                                        " argument(s), got " + std::to_string(nargs));
     for (int i = 0; i < nargs; ++i) {
-        const Param& p = nk.decl.params[i];
+        const Param& p = decl.params[i];
         bool ok;
         if (p.ptr) ok = args[i].kind == TT_ARG_PTR;
         else
@@ -1009,19 +1154,22 @@ tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_ar
                                                            " does not match parameter '" + p.name +
                                                            "' of type " + p.type_text());
     }
-    if (cfg->shared_bytes_extra > ctx->caps.max_shared_bytes)
+    const std::uint64_t shared_total = cfg->shared_bytes_extra + (jit ? jit->prog.static_shared : 0);
+    if (shared_total > ctx->caps.max_shared_bytes)
         return fail(ctx, TT_ERR_LAUNCH_CONFIG, "LaunchConfigError: shared memory of " +
-                                                   std::to_string(cfg->shared_bytes_extra) +
+                                                   std::to_string(shared_total) +
                                                    " bytes exceeds the cap of " +
                                                    std::to_string(ctx->caps.max_shared_bytes));
 
     DeviceGuard guard(ctx->device);
-    LaunchOutcome o = nk.fn(*ctx, *cfg, ra);
+    LaunchOutcome o = native ? native->fn(*ctx, *cfg, ra) : run_jit(*ctx, *jit, *cfg, ra, shared_total);
     if (o.status != TT_OK) return fail(ctx, o.status, o.error);
 
-    if (!o.trap.trapped)
-        for (int i = 0; i < nargs; ++i)
-            if (nk.decl.params[i].written) ++ctx->allocs[args[i].v.ptr.base].gen;
+    // Allocations a launch may have written get a new generation (cached texture / weight copies go
+    // stale): the native kernels' output parameters; every pointer argument of a JIT kernel.
+    for (int i = 0; i < nargs; ++i)
+        if (args[i].kind == TT_ARG_PTR && (native ? (!o.trap.trapped && decl.params[i].written) : true))
+            ++ctx->allocs[args[i].v.ptr.base].gen;
 
     // Counting and the launch log, driver.hpp:235-246 (traps count too).
     ++ctx->c.launches;
@@ -1029,7 +1177,7 @@ tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_ar
     ctx->events.push_back(TT_EV_LAUNCH);
     finish_launch_log(ctx);
     LaunchRecord rec;
-    rec.kernel = nk.decl.name;
+    rec.kernel = decl.name;
     for (int i = 0; i < 3; ++i) {
         rec.grid[i] = cfg->grid[i];
         rec.block[i] = cfg->block[i];
@@ -1614,3 +1762,22 @@ tt_status tt_ipc_close(void* d_ptr) {
 }
 
 }  // extern "C"
+
+extern "C" tt_status tt_jit_source(const char* vptx, std::size_t len, const char* kernel, char* buf, std::size_t cap,
+                                   std::size_t* needed) {
+    if (!vptx || !kernel) return fail(nullptr, TT_ERR_INVALID, "null argument");
+    Module m;
+    tt_status st = parse_module(nullptr, vptx, len, m);
+    if (st != TT_OK) return st;
+    for (const auto& k : m.kernels) {
+        if (k.name != kernel) continue;
+        std::vector<tt::jit::Param> jp;
+        for (const Param& p : k.params) jp.push_back(tt::jit::Param{p.ptr, tt::jit::Ty(static_cast<int>(p.type)), p.name});
+        std::string src, err;
+        std::uint64_t sh = 0;
+        if (!tt::jit::translate(k.name, jp, k.body, src, sh, err))
+            return fail(nullptr, TT_ERR_VALIDATION_FAILED, "ValidationFailed:\n  " + err);
+        return copy_out_text(src, buf, cap, needed);
+    }
+    return fail(nullptr, TT_ERR_FUNCTION_NOT_FOUND, std::string("FunctionNotFound: '") + kernel + "'");
+}
