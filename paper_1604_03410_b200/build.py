@@ -15,8 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtt_b200.so")
 
-SOURCES = ["tt_kernels.cu", "tt_context.cpp", "tt_host.cpp", "tt_jit.cpp"]
-HEADERS = ["tt_kernels.cuh", "tt_jit.h"]
+SOURCES = ["tt_kernels.cu", "tt_context.cpp", "tt_device_api.cpp", "tt_host.cpp", "tt_jit.cpp"]
+HEADERS = ["tt_kernels.cuh", "tt_jit.h", "tt_context_impl.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

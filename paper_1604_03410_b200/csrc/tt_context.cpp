@@ -34,170 +34,43 @@
 #include <cudaTypedefs.h>
 #include <mutex>
 
-#include "tt_b200.h"
-#include "tt_jit.h"
-#include "tt_kernels.cuh"
+#include "tt_context_impl.h"
+
+
+namespace ttc {
 
 namespace {
-
-// ---------------------------------------------------------------- types
-
-enum class Scalar : std::uint8_t { I32, I64, F32, F64 };
-
-const char* scalar_name(Scalar t) {
-    switch (t) {
-        case Scalar::I32: return "i32";
-        case Scalar::I64: return "i64";
-        case Scalar::F32: return "f32";
-        case Scalar::F64: return "f64";
-    }
-    return "?";
-}
-
-std::size_t scalar_bytes(Scalar t) { return (t == Scalar::I64 || t == Scalar::F64) ? 8 : 4; }
-
-// vptx::Param (vptx.hpp:186-199): a by-value scalar or a global pointer.
-struct Param {
-    bool ptr = false;
-    Scalar type = Scalar::I32;
-    std::string name;
-    bool written = false;  // the native kernel stores through this pointer
-    bool operator==(const Param& o) const { return ptr == o.ptr && type == o.type; }
-    std::string type_text() const { return ptr ? std::string("ptr.global.") + scalar_name(type) : scalar_name(type); }
-    std::string sig_text() const { return ptr ? std::string(scalar_name(type)) + "[]" : scalar_name(type); }
-};
-
-struct KernelDecl {
-    std::string name;
-    std::vector<Param> params;
-    std::vector<tt::jit::Line> body;  // instructions / declarations between '{' and '}' (JIT input)
-    std::string signature() const {  // Signature::to_string, types.hpp:104-111
-        std::string s = name + "(";
-        for (std::size_t i = 0; i < params.size(); ++i) {
-            if (i) s += ",";
-            s += params[i].sig_text();
-        }
-        return s + ")";
-    }
-};
-
-struct ResolvedArg {
-    tt_arg_kind kind;
-    tt_arg value;          // scalars
-    void* dptr = nullptr;  // device address for pointers
-    std::uint64_t bytes = 0;
-    std::uint64_t base = 0;  // synthetic address (allocation key)
-    std::uint64_t gen = 0;   // write generation of the allocation
-};
-
-struct LaunchOutcome {
-    tt_status status = TT_OK;
-    std::string error;
-    tt_trap trap{};
-    int gpu_launches = 0;
-};
-using LaunchFn = LaunchOutcome (*)(tt_ctx&, const tt_grid&, const std::vector<ResolvedArg>&);
-
-struct NativeKernel {
-    KernelDecl decl;
-    LaunchFn fn;
-    // The fused trace kernels stand in for their documented DSL bodies (oracle/trace_t05.krn,
-    // bit-exact vs the reference engine) whatever body a module carries; the sample kernels only
-    // bind to header-only modules -- a module with a real VPTX body runs that body (JIT).
-    bool replaces_body = false;
-};
-
-const std::vector<NativeKernel>& registry();
-
-// ---------------------------------------------------------------- context
-
-struct Alloc {
-    void* dptr = nullptr;
-    std::uint64_t bytes = 0;
-    bool live = true;
-    std::uint64_t gen = 0;  // bumped by every write (H2D copy, written launch argument)
-};
-
-// Texture-gather sampler state cached per image allocation: the block-linear
-// cudaArray copy is refreshed only when the allocation's generation changed.
-struct TexEntry {
-    std::uint64_t gen = ~0ull;
-    int n = 0;
-    int batch = 1;
-    int cols = 1;
-    cudaArray_t arr = nullptr;
-    cudaTextureObject_t tex = 0;
-};
-
-// Pass-2 weight layout (tt::launch_weights_soa) cached per wtab allocation,
-// rebuilt only when the allocation's generation changed.
-struct WeightEntry {
-    std::uint64_t gen = ~0ull;
-    int n = 0;
-    float* d = nullptr;
-};
-
-struct LaunchRecord {
-    std::string kernel;
-    std::uint32_t grid[3] = {1, 1, 1};
-    std::uint32_t block[3] = {1, 1, 1};
-    std::uint64_t h2d = 0, d2h = 0;
-};
-
-struct Module {
-    std::string name;
-    std::vector<KernelDecl> kernels;
-};
-
-// A kernel without a native implementation, compiled from its VPTX body (tt_jit.h).
-struct JitFunction {
-    KernelDecl decl;
-    tt::jit::Program prog;
-    ~JitFunction() { tt::jit::release(prog); }
-};
-
-struct FunctionEntry {
-    std::uint64_t module_id = 0;
-    std::string kernel;
-    const NativeKernel* native = nullptr;
-    std::shared_ptr<JitFunction> jit;  // set when native == nullptr
-};
-
 std::atomic<std::uint64_t> g_next_ctx_id{0};
 thread_local std::string t_last_error;
-
 }  // namespace
 
-struct tt_ctx {
-    std::uint64_t id = 0;
-    int device = 0;
-    tt_caps caps{1024, 48 * 1024};
-    bool destroyed = false;
-    cudaStream_t stream = nullptr;
-    int sampler = 1;  // tt::Sampler for trace launches (default texture; TT_SAMPLER=ldg -> 0)
+tt_status fail(const tt_ctx* ctx, tt_status st, const std::string& msg) {
+    if (ctx) const_cast<tt_ctx*>(ctx)->last_error = msg;
+    t_last_error = msg;
+    return st;
+}
 
-    std::map<std::uint64_t, Module> modules;
-    std::map<std::uint64_t, FunctionEntry> functions;
-    std::uint64_t next_handle = 1;
+tt_status cuda_fail(const tt_ctx* ctx, cudaError_t e, const char* what) {
+    return fail(ctx, TT_ERR_CUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
 
-    std::map<std::uint64_t, Alloc> allocs;  // keyed by synthetic base address
-    std::uint64_t bump = 4096;              // GlobalMemory::kBase, emulator.hpp:109
+}  // namespace ttc
 
-    tt_counters c{};
-    std::vector<LaunchRecord> launch_log;
-    std::vector<std::uint8_t> events;
-    std::uint64_t h2d_mark = 0, d2h_mark = 0;
+namespace ttc {
+tt_status copy_out_text(const std::string& s, char* buf, std::size_t cap, std::size_t* needed) {
+    if (needed) *needed = s.size() + 1;
+    if (buf == nullptr || cap == 0) return TT_OK;
+    if (cap < s.size() + 1) return fail(nullptr, TT_ERR_INVALID, "buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return TT_OK;
+}
+}  // namespace ttc
 
-    std::string last_error;
-    std::map<std::uint64_t, TexEntry> tex_cache;      // keyed by image allocation base
-    std::map<std::uint64_t, WeightEntry> w_cache;     // keyed by wtab allocation base
-    // JIT launches: the device trap record and the allocation table the bounds checks search
-    tt::jit::TrapRecord* jit_trap = nullptr;
-    unsigned long long* jit_rng = nullptr;
-    std::size_t jit_rng_cap = 0;  // entries (3 words each)
-};
+using namespace ttc;
 
 namespace {
+
+const std::vector<NativeKernel>& registry();  // the native sm_100a kernels, defined below
 
 void drop_weights(tt_ctx* ctx, std::uint64_t base) {
     auto it = ctx->w_cache.find(base);
@@ -215,35 +88,9 @@ void drop_texture(tt_ctx* ctx, std::uint64_t base) {
     ctx->tex_cache.erase(it);
 }
 
-tt_status fail(const tt_ctx* ctx, tt_status st, const std::string& msg) {
-    if (ctx) const_cast<tt_ctx*>(ctx)->last_error = msg;
-    t_last_error = msg;
-    return st;
-}
 
-tt_status cuda_fail(const tt_ctx* ctx, cudaError_t e, const char* what) {
-    return fail(ctx, TT_ERR_CUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
-}
 
-// Makes the context's device current for the duration of a call.
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-    }
-};
 
-#define TT_CHECK_CTX(ctx)                                                                       \
-    do {                                                                                        \
-        if ((ctx) == nullptr) return fail(nullptr, TT_ERR_INVALID, "null context");            \
-        if ((ctx)->destroyed)                                                                   \
-            return fail((ctx), TT_ERR_CONTEXT_DESTROYED, "ContextDestroyed: operation on a destroyed context"); \
-    } while (0)
 
 void finish_launch_log(tt_ctx* ctx) {  // driver.hpp:322-325
     if (!ctx->launch_log.empty()) ctx->launch_log.back().d2h = ctx->c.bytes_d2h - ctx->d2h_mark;
@@ -683,13 +530,6 @@ const std::vector<NativeKernel>& registry() {
     return reg;
 }
 
-tt_status copy_out_text(const std::string& s, char* buf, std::size_t cap, std::size_t* needed) {
-    if (needed) *needed = s.size() + 1;
-    if (buf == nullptr || cap == 0) return TT_OK;
-    if (cap < s.size() + 1) return fail(nullptr, TT_ERR_INVALID, "buffer too small");
-    std::memcpy(buf, s.c_str(), s.size() + 1);
-    return TT_OK;
-}
 
 std::string json_escape(const std::string& s) {
     std::string o;
@@ -1233,532 +1073,6 @@ tt_status tt_events(tt_ctx* ctx, std::uint8_t* buf, std::size_t cap, std::size_t
     if (cap < ctx->events.size()) return fail(ctx, TT_ERR_INVALID, "buffer too small");
     std::memcpy(buf, ctx->events.data(), ctx->events.size());
     return TT_OK;
-}
-
-// ---- trace-transform helpers -------------------------------------------------
-
-int tt_schedule_slots(int n, int full) { return tt::schedule_slots(n, full != 0); }
-
-tt_status tt_ffma_probe(float* d_out, int blocks, int iters, void* stream) {
-    if (!d_out || blocks < 1 || iters < 1) return fail(nullptr, TT_ERR_INVALID, "bad probe arguments");
-    cudaError_t e = tt::launch_ffma_probe(d_out, blocks, iters, (cudaStream_t)stream);
-    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "ffma probe");
-}
-int tt_max_full_n(void) { return tt::max_full_n(); }
-
-static tt_status check_desc(const tt_trace_desc* d) {
-    if (!d) return fail(nullptr, TT_ERR_INVALID, "null descriptor");
-    if (d->n < 1 || d->n > (d->full ? tt::max_full_n() : 32768))
-        return fail(nullptr, TT_ERR_LAUNCH_CONFIG, "LaunchConfigError: n out of range for the native kernel");
-    if (d->a_count < 0 || d->a0 < 0) return fail(nullptr, TT_ERR_INVALID, "negative angle range");
-    if (d->pair_stride > 0 && d->a_count % 2 != 0)
-        return fail(nullptr, TT_ERR_INVALID, "explicit pair_stride needs an even a_count");
-    if (d->partner_row > 0 && d->batch > 1)
-        return fail(nullptr, TT_ERR_INVALID, "partner_row applies to single-image launches");
-    if ((long long)d->a_count * d->n >= (1ll << 31)) return fail(nullptr, TT_ERR_INVALID, "launch too large");
-    if (d->batch < 0 || d->img_stride < 0) return fail(nullptr, TT_ERR_INVALID, "negative batch or stride");
-    if (d->img_stride != 0 && d->img_stride < (long long)d->n * d->n)
-        return fail(nullptr, TT_ERR_INVALID, "img_stride smaller than one image");
-    if (!d->ctab || !d->stab || !d->out || (d->full && !d->wtab))
-        return fail(nullptr, TT_ERR_INVALID, "null table or output pointer");
-    if (d->full && ((reinterpret_cast<std::uintptr_t>(d->wtab) | reinterpret_cast<std::uintptr_t>(d->wsoa)) & 15u))
-        return fail(nullptr, TT_ERR_INVALID, "wtab / wsoa must be 16-byte aligned");
-    return TT_OK;
-}
-
-static tt::TraceArgs to_args(const tt_trace_desc* d) {
-    tt::TraceArgs ta;
-    ta.img = d->img;
-    ta.n = d->n;
-    ta.a0 = d->a0;
-    if (d->pair_stride == 0) {
-        tt::launch_structure(d->a_count, &ta.a_count, &ta.pair_stride);
-    } else if (d->pair_stride > 0 && d->a_count % 2 == 0) {
-        ta.a_count = d->a_count / 2;
-        ta.pair_stride = d->pair_stride;
-    } else {
-        ta.a_count = d->a_count;
-        ta.pair_stride = 0;
-    }
-    ta.ctab = d->ctab;
-    ta.stab = d->stab;
-    ta.wtab = d->wtab;
-    ta.wsoa = d->wsoa;
-    if (d->partner_row > 0 && ta.pair_stride > 0) ta.partner_row = d->partner_row;
-    ta.peer_out = (d->flags & TT_TRACE_PEER_OUT) != 0;
-    ta.out = d->out;
-    ta.med = d->med;
-    ta.full = d->full != 0;
-    ta.batch = d->batch > 1 ? d->batch : 1;
-    ta.img_stride = d->img_stride;
-    return ta;
-}
-
-// Raw-pointer launches without a prepared weight layout convert wtab into
-// stream-ordered scratch around the launch (one extra small kernel).
-struct WeightScratch {
-    float* d = nullptr;
-    cudaStream_t s = nullptr;
-    ~WeightScratch() {
-        if (d) cudaFreeAsync(d, s);
-    }
-    cudaError_t prepare(tt::TraceArgs& ta, cudaStream_t stream) {
-        if (!ta.full || ta.wsoa) return cudaSuccess;
-        s = stream;
-        cudaError_t e = cudaMallocAsync((void**)&d, tt::weights_soa_bytes(ta.n), stream);
-        if (e != cudaSuccess) return e;
-        ta.wsoa = d;
-        return tt::launch_weights_soa(ta.wtab, ta.n, d, stream);
-    }
-};
-
-tt_status tt_weights_soa(const float* d_wtab, int n, float* d_wsoa, void* stream) {
-    if (!d_wtab || !d_wsoa || n < 1) return fail(nullptr, TT_ERR_INVALID, "bad weight-table arguments");
-    if ((reinterpret_cast<std::uintptr_t>(d_wtab) | reinterpret_cast<std::uintptr_t>(d_wsoa)) & 15u)
-        return fail(nullptr, TT_ERR_INVALID, "weight tables must be 16-byte aligned");
-    cudaError_t e = tt::launch_weights_soa(d_wtab, n, d_wsoa, (cudaStream_t)stream);
-    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "weight table");
-}
-
-tt_status tt_trace_device(const tt_trace_desc* d, void* stream) {
-    tt_status st = check_desc(d);
-    if (st != TT_OK) return st;
-    if (!d->img) return fail(nullptr, TT_ERR_INVALID, "null image");
-    tt::TraceArgs ta = to_args(d);
-    cudaStream_t s = (cudaStream_t)stream;
-    WeightScratch ws;
-    if (cudaError_t e = ws.prepare(ta, s); e != cudaSuccess) return cuda_fail(nullptr, e, "weight table");
-    if (d->sampler == 1) {
-        cudaArray_t arr = nullptr;
-        ta.sampler = tt::Sampler::Texture;
-        cudaError_t e = ta.batch > 1
-                            ? tt::make_image_atlas(ta.img, ta.n, ta.batch, ta.img_stride > 0 ? ta.img_stride
-                                                                                           : (long long)ta.n * ta.n,
-                                                   s, &arr, &ta.tex, &ta.atlas_cols)
-                            : tt::make_image_texture(ta.img, ta.n, s, &arr, &ta.tex);
-        if (e != cudaSuccess) return cuda_fail(nullptr, e, "image texture");
-        e = tt::launch_trace(ta, s);
-        cudaStreamSynchronize(s);
-        cudaDestroyTextureObject(ta.tex);
-        cudaFreeArray(arr);
-        return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "trace kernel");
-    }
-    cudaError_t e = tt::launch_trace(ta, s);
-    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "trace kernel");
-}
-
-}  // extern "C"
-
-struct tt_image_tex {
-    cudaArray_t arr = nullptr;
-    cudaTextureObject_t tex = 0;
-    int n = 0;
-    int batch = 1;
-    int cols = 1;
-};
-
-extern "C" {
-
-tt_status tt_circus_device(const float* d_sino, int n, int rows, float* d_circ, void* stream) {
-    if (!d_sino || !d_circ || n < 1 || rows < 0) return fail(nullptr, TT_ERR_INVALID, "bad circus arguments");
-    cudaError_t e = tt::launch_circus(d_sino, n, rows, d_circ, (cudaStream_t)stream);
-    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "circus");
-}
-
-tt_status tt_image_tex_create(const float* d_img, int n, void* stream, tt_image_tex** out) {
-    if (!d_img || !out || n < 1) return fail(nullptr, TT_ERR_INVALID, "bad argument");
-    auto t = std::make_unique<tt_image_tex>();
-    t->n = n;
-    cudaError_t e = tt::make_image_texture(d_img, n, (cudaStream_t)stream, &t->arr, &t->tex);
-    if (e != cudaSuccess) {
-        if (t->arr) cudaFreeArray(t->arr);
-        return cuda_fail(nullptr, e, "make_image_texture");
-    }
-    *out = t.release();
-    return TT_OK;
-}
-
-tt_status tt_image_atlas_create(const float* d_imgs, int n, int batch, std::int64_t img_stride, void* stream,
-                                tt_image_tex** out) {
-    if (!d_imgs || !out || n < 1 || batch < 1) return fail(nullptr, TT_ERR_INVALID, "bad argument");
-    auto t = std::make_unique<tt_image_tex>();
-    t->n = n;
-    t->batch = batch;
-    cudaError_t e = tt::make_image_atlas(d_imgs, n, batch, img_stride > 0 ? img_stride : (long long)n * n,
-                                         (cudaStream_t)stream, &t->arr, &t->tex, &t->cols);
-    if (e != cudaSuccess) {
-        if (t->arr) cudaFreeArray(t->arr);
-        return cuda_fail(nullptr, e, "make_image_atlas (batch too large for one 2-D texture?)");
-    }
-    *out = t.release();
-    return TT_OK;
-}
-
-tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, std::int64_t img_stride, void* stream) {
-    if (!t || !d_imgs) return fail(nullptr, TT_ERR_INVALID, "bad argument");
-    const long long stride = img_stride > 0 ? img_stride : (long long)t->n * t->n;
-    cudaError_t e;
-    if (t->batch == 1 && t->cols == 1)
-        e = cudaMemcpy2DToArrayAsync(t->arr, 0, 0, d_imgs, std::size_t(t->n) * 4, std::size_t(t->n) * 4,
-                                     std::size_t(t->n), cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
-    else
-        e = tt::fill_image_atlas(t->arr, d_imgs, t->n, t->batch, stride, t->cols, (cudaStream_t)stream);
-    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "image texture update");
-}
-
-tt_status tt_image_tex_destroy(tt_image_tex* t) {
-    if (!t) return TT_OK;
-    cudaDestroyTextureObject(t->tex);
-    cudaFreeArray(t->arr);
-    delete t;
-    return TT_OK;
-}
-
-tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, void* stream) {
-    tt_status st = check_desc(d);
-    if (st != TT_OK) return st;
-    if (!t || t->n != d->n) return fail(nullptr, TT_ERR_INVALID, "texture does not match n");
-    tt::TraceArgs ta = to_args(d);
-    if (ta.batch > t->batch) return fail(nullptr, TT_ERR_INVALID, "batch larger than the texture atlas");
-    ta.sampler = tt::Sampler::Texture;
-    ta.tex = t->tex;
-    ta.atlas_cols = t->cols;
-    WeightScratch ws;
-    if (cudaError_t e = ws.prepare(ta, (cudaStream_t)stream); e != cudaSuccess)
-        return cuda_fail(nullptr, e, "weight table");
-    cudaError_t e = tt::launch_trace(ta, (cudaStream_t)stream);
-    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "trace kernel");
-}
-
-}  // extern "C"
-
-// ----------------------------------------------------------------- plans
-//
-// A plan is the host-to-host form of the path (include/tt_b200.h
-// tt_plan_*): the device tables, image texture and output buffers live for
-// the plan's lifetime, and tt_plan_run pipelines one call.  The fused
-// kernel is launched in angle chunks alternating over two compute streams
-// while a copy stream downloads each finished chunk's sinogram rows (and
-// median rows), so the device-to-host transfer overlaps the remaining
-// chunks; the P-functional stage runs once over the whole sinogram.  The
-// chunked launches write exactly the rows of one whole launch (a chunk is
-// the contiguous unit range [u0, u1) plus its mirror rows, partner_row =
-// U), so the outputs are bit-identical to the single-launch path.
-
-struct tt_plan {
-    tt_ctx* ctx = nullptr;
-    tt_plan_desc d{};
-    int F = 1, units = 0, pair = 0, chunks = 1;
-    float *img = nullptr, *ctab = nullptr, *stab = nullptr, *wtab = nullptr, *wsoa = nullptr;
-    float *out = nullptr, *circ = nullptr;
-    std::int32_t* med = nullptr;
-    cudaArray_t arr = nullptr;
-    cudaTextureObject_t tex = 0;
-    int cols = 1;
-    cudaStream_t sc[2] = {nullptr, nullptr}, sx = nullptr, si = nullptr;
-    std::vector<cudaEvent_t> done;      // per chunk: its rows are final
-    std::vector<cudaEvent_t> uploaded;  // per chunk (batched plans): its images are on the device
-    cudaEvent_t ready = nullptr, traced = nullptr;
-};
-
-namespace {
-
-void plan_release(tt_plan* p) {
-    if (!p) return;
-    DeviceGuard guard(p->ctx->device);
-    for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx, p->si})
-        if (s) cudaStreamSynchronize(s);
-    for (cudaEvent_t e : p->done) cudaEventDestroy(e);
-    for (cudaEvent_t e : p->uploaded) cudaEventDestroy(e);
-    if (p->ready) cudaEventDestroy(p->ready);
-    if (p->traced) cudaEventDestroy(p->traced);
-    if (p->tex) cudaDestroyTextureObject(p->tex);
-    if (p->arr) cudaFreeArray(p->arr);
-    for (void* b : {(void*)p->img, (void*)p->ctab, (void*)p->stab, (void*)p->wtab, (void*)p->wsoa, (void*)p->out,
-                    (void*)p->circ, (void*)p->med})
-        if (b) cudaFree(b);
-    for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx, p->si})
-        if (s) cudaStreamDestroy(s);
-    delete p;
-}
-
-}  // namespace
-
-extern "C" {
-
-tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
-    if (!ctx || ctx->destroyed || !d || !out) return fail(ctx, TT_ERR_INVALID, "bad plan arguments");
-    *out = nullptr;
-    const int n = d->n;
-    if (n < 1 || n > (d->full ? tt::max_full_n() : 32768))
-        return fail(ctx, TT_ERR_LAUNCH_CONFIG, "LaunchConfigError: n out of range for the native kernel");
-    if (d->a_total < 1 || d->a0 < 0 || d->a_count < 1 || d->a0 + d->a_count > d->a_total || d->batch < 0 ||
-        d->chunks < 0 || (d->features && !d->full))
-        return fail(ctx, TT_ERR_INVALID, "bad plan descriptor");
-    if ((long long)d->a_count * n * (d->batch > 1 ? d->batch : 1) >= (1ll << 31))
-        return fail(ctx, TT_ERR_INVALID, "plan too large");
-    DeviceGuard guard(ctx->device);
-    auto p = new tt_plan;
-    p->ctx = ctx;
-    p->d = *d;
-    p->d.batch = d->batch > 1 ? d->batch : 1;
-    p->F = d->full ? tt::kNumF : 1;
-    tt::launch_structure(d->a_count, &p->units, &p->pair);
-    const int B = p->d.batch;
-    // chunks: >= ~1.6e7 unit-taps (~40 us of kernel) each so the per-chunk enqueue cost stays hidden,
-    // at most 32 (measured on C2: 5 chunks 1.28 ms, 24-32 chunks 1.24 ms; C1 best unchunked)
-    int ch = d->chunks;
-    if (ch == 0) ch = int(std::max(1LL, std::min(32LL, (long long)p->units * B * n * n / 16000000LL)));
-    p->chunks = std::max(1, std::min(ch, B > 1 ? B : p->units));  // angle chunks (one image) or image chunks
-    const std::size_t N2 = std::size_t(n) * n;
-    const std::size_t rows = std::size_t(B) * d->a_count;
-    cudaError_t e = cudaSuccess;
-    auto alloc = [&](auto** ptr, std::size_t bytes) {
-        if (e == cudaSuccess) e = cudaMalloc((void**)ptr, bytes ? bytes : 4);
-    };
-    alloc(&p->img, B * N2 * 4);
-    alloc(&p->ctab, std::size_t(d->a_total) * 4);
-    alloc(&p->stab, std::size_t(d->a_total) * 4);
-    alloc(&p->out, rows * p->F * n * 4);
-    if (d->full) {
-        alloc(&p->wtab, std::size_t(n) * 32);
-        alloc(&p->wsoa, tt::weights_soa_bytes(n));
-        alloc(&p->med, rows * 2 * n * 4);
-    }
-    if (d->features) alloc(&p->circ, rows * tt::kNumF * 3 * 4);
-    for (cudaStream_t* s : {&p->sc[0], &p->sc[1], &p->sx, &p->si})
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
-    p->done.resize(p->chunks, nullptr);
-    p->uploaded.resize(p->chunks, nullptr);
-    for (auto* evs : {&p->done, &p->uploaded})
-        for (auto& ev : *evs)
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->traced, cudaEventDisableTiming);
-    if (e != cudaSuccess) {
-        plan_release(p);
-        return cuda_fail(ctx, e, "plan buffers");
-    }
-    // tables (host f64 -> f32, spec §2.1-2.2), the pass-2 weight layout, the image texture
-    std::vector<float> ct(d->a_total), st(d->a_total), wt(d->full ? std::size_t(n) * 8 : 0);
-    tt_make_tables(n, d->a_total, ct.data(), st.data(), d->full ? wt.data() : nullptr);
-    e = cudaMemcpyAsync(p->ctab, ct.data(), ct.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(p->stab, st.data(), st.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
-    if (e == cudaSuccess && d->full) {
-        e = cudaMemcpyAsync(p->wtab, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
-        if (e == cudaSuccess) e = tt::launch_weights_soa(p->wtab, n, p->wsoa, p->sc[0]);
-    }
-    if (e == cudaSuccess && ctx->sampler == int(tt::Sampler::Texture))
-        e = B > 1 ? tt::make_image_atlas(p->img, n, B, (long long)N2, p->sc[0], &p->arr, &p->tex, &p->cols)
-                  : tt::make_image_texture(p->img, n, p->sc[0], &p->arr, &p->tex);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(p->sc[0]);
-    if (e != cudaSuccess) {
-        plan_release(p);
-        return cuda_fail(ctx, e, "plan setup");
-    }
-    *out = p;
-    return TT_OK;
-}
-
-tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t* h_med, float* h_circ) {
-    if (!p || !h_img) return fail(p ? p->ctx : nullptr, TT_ERR_INVALID, "bad plan run arguments");
-    tt_ctx* ctx = p->ctx;
-    if (ctx->destroyed) return fail(ctx, TT_ERR_INVALID, "context destroyed");
-    DeviceGuard guard(ctx->device);
-    const tt_plan_desc& d = p->d;
-    const int n = d.n, B = d.batch, F = p->F;
-    const std::size_t N2 = std::size_t(n) * n;
-    const std::size_t row_f = std::size_t(F) * n, row_m = 2 * std::size_t(n), row_c = std::size_t(tt::kNumF) * 3;
-    cudaError_t e = cudaSuccess;
-    std::uint64_t h2d = 0, d2h = 0, launches = 0;
-    auto ok = [&](cudaError_t x) {
-        if (e == cudaSuccess) e = x;
-        return e == cudaSuccess;
-    };
-    const bool tex = ctx->sampler == int(tt::Sampler::Texture);
-    auto trace_args = [&](int u0, int u1, int b0, int b1) {
-        tt::TraceArgs ta;
-        ta.img = p->img;
-        ta.tex = p->tex;
-        ta.sampler = tex ? tt::Sampler::Texture : tt::Sampler::Global;
-        ta.atlas_cols = p->cols;
-        ta.n = n;
-        ta.a0 = d.a0 + u0;
-        ta.a_count = u1 - u0;
-        ta.pair_stride = p->pair;
-        ta.partner_row = B == 1 ? p->units : -1;  // angle chunks write their mirror rows at U (one image)
-        ta.ctab = p->ctab;
-        ta.stab = p->stab;
-        ta.wtab = p->wtab;
-        ta.wsoa = p->wsoa;
-        const std::size_t rows0 = std::size_t(b0) * d.a_count + u0;  // first output row of the launch
-        ta.out = p->out + rows0 * row_f;
-        ta.med = d.full ? p->med + rows0 * row_m : nullptr;
-        ta.full = d.full != 0;
-        ta.batch = b1 - b0;
-        ta.img0 = b0;
-        return ta;
-    };
-    auto download = [&](std::size_t r0, std::size_t cnt) {  // output rows [r0, r0 + cnt) on the copy stream
-        if (h_out) {
-            ok(cudaMemcpyAsync(h_out + r0 * row_f, p->out + r0 * row_f, cnt * row_f * 4, cudaMemcpyDeviceToHost, p->sx));
-            d2h += cnt * row_f * 4;
-        }
-        if (h_med && d.full) {
-            ok(cudaMemcpyAsync(h_med + r0 * row_m, p->med + r0 * row_m, cnt * row_m * 4, cudaMemcpyDeviceToHost, p->sx));
-            d2h += cnt * row_m * 4;
-        }
-    };
-    if (B == 1) {
-        // 1. image in (straight into the texture array when the sampler reads only the texture)
-        if (tex)
-            ok(cudaMemcpy2DToArrayAsync(p->arr, 0, 0, h_img, std::size_t(n) * 4, std::size_t(n) * 4, std::size_t(n),
-                                        cudaMemcpyHostToDevice, p->sc[0]));
-        else
-            ok(cudaMemcpyAsync(p->img, h_img, N2 * 4, cudaMemcpyHostToDevice, p->sc[0]));
-        h2d += N2 * 4;
-        ok(cudaEventRecord(p->ready, p->sc[0]));
-        ok(cudaStreamWaitEvent(p->sc[1], p->ready, 0));
-        // 2. angle chunks alternating over two compute streams; each finished chunk's forward and
-        //    mirror rows go out on the copy stream while later chunks compute
-        for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
-            const int u0 = int((long long)p->units * c / p->chunks), u1 = int((long long)p->units * (c + 1) / p->chunks);
-            cudaStream_t s = p->sc[c & 1];
-            tt::TraceArgs ta = trace_args(u0, u1, 0, 1);
-            if (!ok(tt::launch_trace(ta, s))) break;
-            launches += tt::trace_launch_count(ta);
-            ok(cudaEventRecord(p->done[c], s));
-            if (h_out || h_med) {
-                ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
-                for (int half = 0; half < (p->pair ? 2 : 1); ++half) download(std::size_t(u0 + half * p->units), u1 - u0);
-            }
-        }
-        for (int c = 0; c < p->chunks; ++c) ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
-        if (d.features) {  // 3. P-functionals over the whole sinogram
-            const std::size_t rows = d.a_count;
-            ok(tt::launch_circus(p->out, n, int(rows * tt::kNumF), p->circ, p->sx));
-            ++launches;
-            if (h_circ) {
-                ok(cudaMemcpyAsync(h_circ, p->circ, rows * row_c * 4, cudaMemcpyDeviceToHost, p->sx));
-                d2h += rows * row_c * 4;
-            }
-        }
-    } else {
-        // Image chunks: chunk c's upload (copy-in stream) overlaps chunk c-1's trace + features
-        // (compute stream) and chunk c-2's download (copy-out stream).
-        const int units_all = d.a_count;  // rows per image
-        for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
-            const int b0 = int((long long)B * c / p->chunks), b1 = int((long long)B * (c + 1) / p->chunks);
-            const std::size_t cnt = std::size_t(b1 - b0);
-            ok(cudaMemcpyAsync(p->img + b0 * N2, h_img + b0 * N2, cnt * N2 * 4, cudaMemcpyHostToDevice, p->si));
-            h2d += cnt * N2 * 4;
-            ok(cudaEventRecord(p->uploaded[c], p->si));
-            cudaStream_t s = p->sc[0];
-            ok(cudaStreamWaitEvent(s, p->uploaded[c], 0));
-            if (tex) {
-                ok(tt::fill_image_atlas(p->arr, p->img + b0 * N2, n, int(cnt), (long long)N2, p->cols, s, b0));
-                ++launches;
-            }
-            tt::TraceArgs ta = trace_args(0, p->units, b0, b1);
-            if (!ok(tt::launch_trace(ta, s))) break;
-            launches += tt::trace_launch_count(ta);
-            const std::size_t r0 = std::size_t(b0) * units_all, rows = cnt * units_all;
-            if (d.features) {
-                ok(tt::launch_circus(p->out + r0 * row_f, n, int(rows * tt::kNumF), p->circ + r0 * row_c, s));
-                ++launches;
-            }
-            ok(cudaEventRecord(p->done[c], s));
-            ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
-            download(r0, rows);
-            if (d.features && h_circ) {
-                ok(cudaMemcpyAsync(h_circ + r0 * row_c, p->circ + r0 * row_c, rows * row_c * 4, cudaMemcpyDeviceToHost,
-                                   p->sx));
-                d2h += rows * row_c * 4;
-            }
-        }
-    }
-    ok(cudaStreamSynchronize(p->sx));
-    ok(cudaStreamSynchronize(p->si));
-    ok(cudaStreamSynchronize(p->sc[0]));
-    ok(cudaStreamSynchronize(p->sc[1]));
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "plan run");
-    ctx->c.bytes_h2d += h2d;
-    ctx->c.bytes_d2h += d2h;
-    ctx->c.gpu_kernel_launches += launches;
-    return TT_OK;
-}
-
-tt_status tt_plan_chunks(const tt_plan* p, int* chunks) {
-    if (!p || !chunks) return fail(nullptr, TT_ERR_INVALID, "null argument");
-    *chunks = p->chunks;
-    return TT_OK;
-}
-
-tt_status tt_plan_destroy(tt_plan* p) {
-    plan_release(p);
-    return TT_OK;
-}
-
-}  // extern "C"
-
-// ------------------------------------------------------------------- IPC
-
-namespace {
-std::mutex g_ipc_mu;
-std::map<void*, void*> g_ipc_open;  // imported pointer (base + offset) -> mapped base
-}  // namespace
-
-extern "C" {
-
-tt_status tt_ipc_export(const void* d_ptr, tt_ipc_handle* out) {
-    if (!d_ptr || !out) return fail(nullptr, TT_ERR_INVALID, "null argument");
-    static PFN_cuMemGetAddressRange_v3020 range = [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            f = nullptr;
-        return reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(f);
-    }();
-    if (!range) return fail(nullptr, TT_ERR_CUDA, "cuMemGetAddressRange unavailable");
-    CUdeviceptr base = 0;
-    size_t size = 0;
-    if (range(&base, &size, CUdeviceptr(d_ptr)) != CUDA_SUCCESS)
-        return fail(nullptr, TT_ERR_INVALID, "pointer is not inside a device allocation");
-    cudaIpcMemHandle_t h;
-    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
-    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaIpcGetMemHandle");
-    static_assert(sizeof(h) == sizeof(out->bytes), "IPC handle size");
-    std::memcpy(out->bytes, &h, sizeof(h));
-    out->offset = std::uint64_t(CUdeviceptr(d_ptr) - base);
-    return TT_OK;
-}
-
-tt_status tt_ipc_import(const tt_ipc_handle* hd, int device, void** d_ptr) {
-    if (!hd || !d_ptr) return fail(nullptr, TT_ERR_INVALID, "null argument");
-    DeviceGuard guard(device);
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, hd->bytes, sizeof(h));
-    void* base = nullptr;
-    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaIpcOpenMemHandle");
-    *d_ptr = static_cast<char*>(base) + hd->offset;
-    std::lock_guard<std::mutex> lk(g_ipc_mu);
-    g_ipc_open[*d_ptr] = base;
-    return TT_OK;
-}
-
-tt_status tt_ipc_close(void* d_ptr) {
-    void* base = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(g_ipc_mu);
-        auto it = g_ipc_open.find(d_ptr);
-        if (it == g_ipc_open.end()) return fail(nullptr, TT_ERR_INVALID, "pointer was not imported");
-        base = it->second;
-        g_ipc_open.erase(it);
-    }
-    cudaError_t e = cudaIpcCloseMemHandle(base);
-    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "cudaIpcCloseMemHandle");
 }
 
 }  // extern "C"
