@@ -306,6 +306,32 @@ static float replay_strided_sum(const float* v, int len, int NS) {
 static int replay_rescan(const float* u, int n, int start, int K, float exc, float S, int LG) {
     int len = n - start;
     if (len > K) len = K;
+    if (LG < 32 && (K == 4 * LG || K == 2 * LG)) {
+        /* sub-warp segments: lane q holds E = K/LG consecutive elements, sequential
+         * in-lane prefix l_e, Kogge-Stone over the lane totals, P = exc + (X_q + l_e)
+         * (kernel rescan_lanes) */
+        const int E = K / LG;
+        float l[32][4], T[32];
+        for (int q = 0; q < LG; ++q) {
+            for (int e = 0; e < E; ++e) {
+                const int j = q * E + e;
+                const float x = (j < len) ? u[start + j] : 0.0f;
+                l[q][e] = e == 0 ? x : l[q][e - 1] + x;
+            }
+            T[q] = l[q][E - 1];
+        }
+        warp_scan(T, LG);
+        for (int q = 0; q < LG; ++q) {
+            const float X = q == 0 ? 0.0f : T[q - 1];
+            for (int e = 0; e < E; ++e) {
+                const int j = q * E + e;
+                if (j >= len) continue;
+                const float P = exc + (X + l[q][e]);
+                if (P + P >= S) return start + j;
+            }
+        }
+        return len > 0 ? start + len - 1 : n - 1;
+    }
     float C = 0.0f;
     for (int b = 0; b * LG < len; ++b) {
         float x[32];
