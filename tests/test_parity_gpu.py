@@ -285,3 +285,28 @@ def test_prepared_weight_layout_equals_per_call_conversion(ctx, n, A):
     for b in list(bufs.values()) + [ws, out_d, med_d]:
         ctx.mem_free(b)
     assert _bitwise_equal(out, ref) and np.array_equal(med, rmed)
+
+
+def _random_configs(count=24, seed=20260417):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        n = int(rng.choice([int(rng.integers(2, 700)), int(2 ** rng.integers(3, 11))]))
+        A = int(rng.integers(1, 40))
+        a0 = int(rng.integers(0, A))
+        cnt = int(rng.integers(1, A - a0 + 1))
+        out.append((n, A, a0, cnt, int(rng.integers(0, 3)), int(rng.integers(0, 2)), bool(rng.integers(0, 2))))
+    return out
+
+
+@pytest.mark.parametrize("n,A,a0,cnt,kind,sampler,full", _random_configs())
+def test_random_configurations_bit_exact_vs_replay(ctx, n, A, a0, cnt, kind, sampler, full):
+    """Seeded random sizes / angle ranges / images / samplers / functional sets."""
+    img = tt.synth_image([tt.DISK, tt.PHANTOM, tt.SPARSE][kind], n)
+    tr, out, med = _run(ctx, img, n, A, full=full, sampler=sampler, a0=a0, a_count=cnt)
+    rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, a0=a0, a_count=cnt, mode=O.REPLAY, full=full)
+    assert _bitwise_equal(out, rout)
+    if full:
+        assert np.array_equal(med, rmed)
+    fails, st = O.check(img, n, tr.ctab, tr.stab, tr.wtab, out, med if full else None, a0=a0, full=full)
+    assert fails == 0, st
