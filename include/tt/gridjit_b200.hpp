@@ -417,4 +417,46 @@ inline LaunchReport cuda_launch(DeviceContext& ctx, const KernelAst& kernel, con
     return rep;
 }
 
+
+// ---- B200 extensions (no reference counterpart) -------------------------------------
+namespace b200 {
+
+// Host-to-host pipelined trace transform (tt_plan_*): tables, texture and outputs stay on
+// the device; run() overlaps the downloads of finished angle chunks with the remaining
+// launches and fills the host buffers (pinned: tt_host_alloc) -- the caller-side loop of
+// cuda_launch (autolaunch.hpp:167-245) over many images of one configuration.
+class TracePlan {
+  public:
+    TracePlan(DeviceContext& ctx, int n, int angles, bool full = true, bool features = false, int a0 = 0,
+              int a_count = -1, int batch = 1, int chunks = 0)
+        : ctx_(ctx.raw()) {
+        tt_plan_desc d{n, angles, a0, a_count < 0 ? angles - a0 : a_count, full ? 1 : 0, features ? 1 : 0,
+                       batch, chunks};
+        detail::check(tt_plan_create(ctx_, &d, &p_), ctx_);
+    }
+    TracePlan(const TracePlan&) = delete;
+    TracePlan& operator=(const TracePlan&) = delete;
+    ~TracePlan() { tt_plan_destroy(p_); }
+
+    // img [batch][n][n]; out [batch][a_count][F][n], med [batch][a_count][2][n],
+    // circ [batch][a_count][6][3] -- any output may be nullptr (not downloaded).
+    void run(const float* img, float* out, std::int32_t* med = nullptr, float* circ = nullptr) {
+        detail::check(tt_plan_run(p_, img, out, med, circ), ctx_);
+    }
+    int chunks() const {
+        int c = 0;
+        tt_plan_chunks(p_, &c);
+        return c;
+    }
+
+  private:
+    tt_ctx* ctx_ = nullptr;
+    tt_plan* p_ = nullptr;
+};
+
+// Side of the square whose inscribed disk holds an h x w picture (tt_prep_side).
+inline int prep_side(int h, int w) { return tt_prep_side(h, w); }
+
+}  // namespace b200
+
 }  // namespace gridjit

@@ -107,6 +107,16 @@ int main() {
         CHECK(std::memcmp(out.data(), ref.data(), out.size() * 4) == 0);
         CHECK(med == rmed);
         CHECK(ctx.counters().gpu_kernel_launches == 2);  // pass-2 weight layout of the uploaded wtab + fused kernel
+
+        // the same transform through the pipelined host-to-host plan: identical bits
+        b200::TracePlan plan(ctx, n, A, true, false, 0, -1, 1, 5);
+        std::vector<float> out2(out.size(), -1.0f);
+        std::vector<std::int32_t> med2(med.size(), -1);
+        plan.run(img.data(), out2.data(), med2.data());
+        CHECK(plan.chunks() == 5);
+        CHECK(std::memcmp(out2.data(), out.data(), out.size() * 4) == 0);
+        CHECK(med2 == med);
+        CHECK(b200::prep_side(480, 640) == 801);
     }
     std::printf("%s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
     return failures ? 1 : 0;
