@@ -428,10 +428,10 @@ namespace b200 {
 class TracePlan {
   public:
     TracePlan(DeviceContext& ctx, int n, int angles, bool full = true, bool features = false, int a0 = 0,
-              int a_count = -1, int batch = 1, int chunks = 0)
+              int a_count = -1, int batch = 1, int chunks = 0, int slots = 0)
         : ctx_(ctx.raw()) {
         tt_plan_desc d{n, angles, a0, a_count < 0 ? angles - a0 : a_count, full ? 1 : 0, features ? 1 : 0,
-                       batch, chunks};
+                       batch, chunks, slots};
         detail::check(tt_plan_create(ctx_, &d, &p_), ctx_);
     }
     TracePlan(const TracePlan&) = delete;
@@ -443,6 +443,11 @@ class TracePlan {
     void run(const float* img, float* out, std::int32_t* med = nullptr, float* circ = nullptr) {
         detail::check(tt_plan_run(p_, img, out, med, circ), ctx_);
     }
+    // Asynchronous form: buffers must stay valid until wait(); consecutive submissions overlap.
+    void submit(const float* img, float* out, std::int32_t* med = nullptr, float* circ = nullptr) {
+        detail::check(tt_plan_submit(p_, img, out, med, circ), ctx_);
+    }
+    void wait() { detail::check(tt_plan_wait(p_), ctx_); }
     int chunks() const {
         int c = 0;
         tt_plan_chunks(p_, &c);

@@ -339,11 +339,19 @@ typedef struct tt_plan_desc {
     int32_t batch;    /* images per run (0 or 1: one) */
     int32_t chunks;   /* pipeline chunks: angle chunks (one image) or image chunks (batch);
                          0 = automatic */
+    int32_t slots;    /* device buffer sets for overlapping submissions (1..4; 0: 2 for one
+                         image, 1 for batches) */
 } tt_plan_desc;
 tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out);
 /* h_img [batch][n][n]; h_out [batch][a_count][F][n], h_med [batch][a_count][2][n],
  * h_circ [batch][a_count][6][3] -- each output may be NULL (not downloaded). */
 tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, int32_t* h_med, float* h_circ);
+/* Asynchronous form: submit enqueues one image (or batch) on the plan's next buffer slot and
+ * returns; its host buffers must stay valid until tt_plan_wait, which drains every submission.
+ * With two slots consecutive submissions overlap (the next upload with the current kernels,
+ * the current downloads with the next kernels).  tt_plan_run = submit + wait. */
+tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, int32_t* h_med, float* h_circ);
+tt_status tt_plan_wait(tt_plan* p);
 tt_status tt_plan_chunks(const tt_plan* p, int* chunks);
 tt_status tt_plan_destroy(tt_plan* p);
 

@@ -49,7 +49,8 @@ class Counters(C.Structure):
 
 
 class PlanDesc(C.Structure):
-    _fields_ = [(k, C.c_int32) for k in ("n", "a_total", "a0", "a_count", "full", "features", "batch", "chunks")]
+    _fields_ = [(k, C.c_int32) for k in ("n", "a_total", "a0", "a_count", "full", "features", "batch", "chunks",
+                                         "slots")]
 
 
 class TraceDesc(C.Structure):
@@ -121,6 +122,8 @@ _sigs = {
     "tt_jit_source": (_S, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "tt_plan_create": (_S, [C.c_void_p, C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]),
     "tt_plan_run": (_S, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tt_plan_submit": (_S, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tt_plan_wait": (_S, [C.c_void_p]),
     "tt_plan_chunks": (_S, [C.c_void_p, C.POINTER(C.c_int)]),
     "tt_plan_destroy": (_S, [C.c_void_p]),
 }

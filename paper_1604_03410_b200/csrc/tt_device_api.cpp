@@ -217,30 +217,40 @@ tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, voi
 // ----------------------------------------------------------------- plans
 //
 // A plan is the host-to-host form of the path (include/tt_b200.h
-// tt_plan_*): the device tables, image texture and output buffers live for
-// the plan's lifetime, and tt_plan_run pipelines one call.  The fused
-// kernel is launched in angle chunks alternating over two compute streams
-// while a copy stream downloads each finished chunk's sinogram rows (and
-// median rows), so the device-to-host transfer overlaps the remaining
-// chunks; the P-functional stage runs once over the whole sinogram.  The
-// chunked launches write exactly the rows of one whole launch (a chunk is
-// the contiguous unit range [u0, u1) plus its mirror rows, partner_row =
-// U), so the outputs are bit-identical to the single-launch path.
+// tt_plan_*): the device tables live for the plan's lifetime and each of
+// its `slots` owns an image texture and output buffers.  tt_plan_submit
+// enqueues one image (or batch) on the next slot and returns; tt_plan_wait
+// drains everything submitted; tt_plan_run = submit + wait.  One image: the
+// fused kernel runs in angle chunks alternating over two compute streams
+// while a copy stream downloads each finished chunk's sinogram and median
+// rows; the P-functional stage runs once over the sinogram.  With two slots
+// the next submission's upload overlaps the current kernels and the current
+// downloads overlap the next kernels.  The chunked launches write exactly
+// the rows of one whole launch (a chunk is the unit range [u0, u1) plus its
+// mirror rows at partner_row = U), so outputs are bit-identical to the
+// single-launch path.  Batched plans chunk by images (upload / atlas fill +
+// trace + features / download on three streams).
 
-struct tt_plan {
-    tt_ctx* ctx = nullptr;
-    tt_plan_desc d{};
-    int F = 1, units = 0, pair = 0, chunks = 1;
-    float *img = nullptr, *ctab = nullptr, *stab = nullptr, *wtab = nullptr, *wsoa = nullptr;
+struct PlanSlot {
+    float* img = nullptr;  // linear image(s) (LDG sampler, batched atlas fill)
     float *out = nullptr, *circ = nullptr;
     std::int32_t* med = nullptr;
     cudaArray_t arr = nullptr;
     cudaTextureObject_t tex = 0;
-    int cols = 1;
-    cudaStream_t sc[2] = {nullptr, nullptr}, sx = nullptr, si = nullptr;
     std::vector<cudaEvent_t> done;      // per chunk: its rows are final
     std::vector<cudaEvent_t> uploaded;  // per chunk (batched plans): its images are on the device
-    cudaEvent_t ready = nullptr, traced = nullptr;
+    cudaEvent_t ready = nullptr;        // image uploaded (single-image plans)
+    cudaEvent_t free = nullptr;         // the slot's last download finished: buffers reusable
+    bool used = false;
+};
+
+struct tt_plan {
+    tt_ctx* ctx = nullptr;
+    tt_plan_desc d{};
+    int F = 1, units = 0, pair = 0, chunks = 1, cols = 1, next = 0;
+    float *ctab = nullptr, *stab = nullptr, *wtab = nullptr, *wsoa = nullptr;
+    std::vector<PlanSlot> slot;
+    cudaStream_t sc[2] = {nullptr, nullptr}, sx = nullptr, si = nullptr;
 };
 
 namespace {
@@ -250,14 +260,18 @@ void plan_release(tt_plan* p) {
     DeviceGuard guard(p->ctx->device);
     for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx, p->si})
         if (s) cudaStreamSynchronize(s);
-    for (cudaEvent_t e : p->done) cudaEventDestroy(e);
-    for (cudaEvent_t e : p->uploaded) cudaEventDestroy(e);
-    if (p->ready) cudaEventDestroy(p->ready);
-    if (p->traced) cudaEventDestroy(p->traced);
-    if (p->tex) cudaDestroyTextureObject(p->tex);
-    if (p->arr) cudaFreeArray(p->arr);
-    for (void* b : {(void*)p->img, (void*)p->ctab, (void*)p->stab, (void*)p->wtab, (void*)p->wsoa, (void*)p->out,
-                    (void*)p->circ, (void*)p->med})
+    for (PlanSlot& sl : p->slot) {
+        for (auto* evs : {&sl.done, &sl.uploaded})
+            for (cudaEvent_t e : *evs)
+                if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : {sl.ready, sl.free})
+            if (e) cudaEventDestroy(e);
+        if (sl.tex) cudaDestroyTextureObject(sl.tex);
+        if (sl.arr) cudaFreeArray(sl.arr);
+        for (void* b : {(void*)sl.img, (void*)sl.out, (void*)sl.circ, (void*)sl.med})
+            if (b) cudaFree(b);
+    }
+    for (void* b : {(void*)p->ctab, (void*)p->stab, (void*)p->wtab, (void*)p->wsoa})
         if (b) cudaFree(b);
     for (cudaStream_t s : {p->sc[0], p->sc[1], p->sx, p->si})
         if (s) cudaStreamDestroy(s);
@@ -275,7 +289,7 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
     if (n < 1 || n > (d->full ? tt::max_full_n() : 32768))
         return fail(ctx, TT_ERR_LAUNCH_CONFIG, "LaunchConfigError: n out of range for the native kernel");
     if (d->a_total < 1 || d->a0 < 0 || d->a_count < 1 || d->a0 + d->a_count > d->a_total || d->batch < 0 ||
-        d->chunks < 0 || (d->features && !d->full))
+        d->chunks < 0 || d->slots < 0 || d->slots > 4 || (d->features && !d->full))
         return fail(ctx, TT_ERR_INVALID, "bad plan descriptor");
     if ((long long)d->a_count * n * (d->batch > 1 ? d->batch : 1) >= (1ll << 31))
         return fail(ctx, TT_ERR_INVALID, "plan too large");
@@ -292,36 +306,44 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
     int ch = d->chunks;
     if (ch == 0) ch = int(std::max(1LL, std::min(32LL, (long long)p->units * B * n * n / 16000000LL)));
     p->chunks = std::max(1, std::min(ch, B > 1 ? B : p->units));  // angle chunks (one image) or image chunks
+    const int nslots = d->slots > 0 ? d->slots : (B > 1 ? 1 : 2);
+    p->d.slots = nslots;
+    p->slot.resize(nslots);
     const std::size_t N2 = std::size_t(n) * n;
     const std::size_t rows = std::size_t(B) * d->a_count;
     cudaError_t e = cudaSuccess;
     auto alloc = [&](auto** ptr, std::size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc((void**)ptr, bytes ? bytes : 4);
     };
-    alloc(&p->img, B * N2 * 4);
     alloc(&p->ctab, std::size_t(d->a_total) * 4);
     alloc(&p->stab, std::size_t(d->a_total) * 4);
-    alloc(&p->out, rows * p->F * n * 4);
     if (d->full) {
         alloc(&p->wtab, std::size_t(n) * 32);
         alloc(&p->wsoa, tt::weights_soa_bytes(n));
-        alloc(&p->med, rows * 2 * n * 4);
     }
-    if (d->features) alloc(&p->circ, rows * tt::kNumF * 3 * 4);
     for (cudaStream_t* s : {&p->sc[0], &p->sc[1], &p->sx, &p->si})
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
-    p->done.resize(p->chunks, nullptr);
-    p->uploaded.resize(p->chunks, nullptr);
-    for (auto* evs : {&p->done, &p->uploaded})
-        for (auto& ev : *evs)
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->traced, cudaEventDisableTiming);
+    for (PlanSlot& sl : p->slot) {
+        alloc(&sl.img, B * N2 * 4);
+        alloc(&sl.out, rows * p->F * n * 4);
+        if (d->full) alloc(&sl.med, rows * 2 * n * 4);
+        if (d->features) alloc(&sl.circ, rows * tt::kNumF * 3 * 4);
+        sl.done.resize(p->chunks, nullptr);
+        sl.uploaded.resize(p->chunks, nullptr);
+        for (auto* evs : {&sl.done, &sl.uploaded})
+            for (auto& ev : *evs)
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        for (cudaEvent_t* ev : {&sl.ready, &sl.free})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (e == cudaSuccess && ctx->sampler == int(tt::Sampler::Texture))
+            e = B > 1 ? tt::make_image_atlas(sl.img, n, B, (long long)N2, p->sc[0], &sl.arr, &sl.tex, &p->cols)
+                      : tt::make_image_texture(sl.img, n, p->sc[0], &sl.arr, &sl.tex);
+    }
     if (e != cudaSuccess) {
         plan_release(p);
         return cuda_fail(ctx, e, "plan buffers");
     }
-    // tables (host f64 -> f32, spec §2.1-2.2), the pass-2 weight layout, the image texture
+    // tables (host f64 -> f32, spec §2.1-2.2) and the pass-2 weight layout
     std::vector<float> ct(d->a_total), st(d->a_total), wt(d->full ? std::size_t(n) * 8 : 0);
     tt_make_tables(n, d->a_total, ct.data(), st.data(), d->full ? wt.data() : nullptr);
     e = cudaMemcpyAsync(p->ctab, ct.data(), ct.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
@@ -330,9 +352,6 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
         e = cudaMemcpyAsync(p->wtab, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
         if (e == cudaSuccess) e = tt::launch_weights_soa(p->wtab, n, p->wsoa, p->sc[0]);
     }
-    if (e == cudaSuccess && ctx->sampler == int(tt::Sampler::Texture))
-        e = B > 1 ? tt::make_image_atlas(p->img, n, B, (long long)N2, p->sc[0], &p->arr, &p->tex, &p->cols)
-                  : tt::make_image_texture(p->img, n, p->sc[0], &p->arr, &p->tex);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->sc[0]);
     if (e != cudaSuccess) {
         plan_release(p);
@@ -342,7 +361,7 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
     return TT_OK;
 }
 
-tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t* h_med, float* h_circ) {
+tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int32_t* h_med, float* h_circ) {
     if (!p || !h_img) return fail(p ? p->ctx : nullptr, TT_ERR_INVALID, "bad plan run arguments");
     tt_ctx* ctx = p->ctx;
     if (ctx->destroyed) return fail(ctx, TT_ERR_INVALID, "context destroyed");
@@ -351,6 +370,8 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
     const int n = d.n, B = d.batch, F = p->F;
     const std::size_t N2 = std::size_t(n) * n;
     const std::size_t row_f = std::size_t(F) * n, row_m = 2 * std::size_t(n), row_c = std::size_t(tt::kNumF) * 3;
+    PlanSlot& sl = p->slot[p->next];
+    p->next = (p->next + 1) % int(p->slot.size());
     cudaError_t e = cudaSuccess;
     std::uint64_t h2d = 0, d2h = 0, launches = 0;
     auto ok = [&](cudaError_t x) {
@@ -358,10 +379,14 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
         return e == cudaSuccess;
     };
     const bool tex = ctx->sampler == int(tt::Sampler::Texture);
+    // the slot's previous submission must have fully drained (its kernels read the texture,
+    // its downloads read the outputs) before this one overwrites them
+    if (sl.used) ok(cudaStreamWaitEvent(p->si, sl.free, 0));
+    sl.used = true;
     auto trace_args = [&](int u0, int u1, int b0, int b1) {
         tt::TraceArgs ta;
-        ta.img = p->img;
-        ta.tex = p->tex;
+        ta.img = sl.img;
+        ta.tex = sl.tex;
         ta.sampler = tex ? tt::Sampler::Texture : tt::Sampler::Global;
         ta.atlas_cols = p->cols;
         ta.n = n;
@@ -374,8 +399,8 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
         ta.wtab = p->wtab;
         ta.wsoa = p->wsoa;
         const std::size_t rows0 = std::size_t(b0) * d.a_count + u0;  // first output row of the launch
-        ta.out = p->out + rows0 * row_f;
-        ta.med = d.full ? p->med + rows0 * row_m : nullptr;
+        ta.out = sl.out + rows0 * row_f;
+        ta.med = d.full ? sl.med + rows0 * row_m : nullptr;
         ta.full = d.full != 0;
         ta.batch = b1 - b0;
         ta.img0 = b0;
@@ -383,24 +408,25 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
     };
     auto download = [&](std::size_t r0, std::size_t cnt) {  // output rows [r0, r0 + cnt) on the copy stream
         if (h_out) {
-            ok(cudaMemcpyAsync(h_out + r0 * row_f, p->out + r0 * row_f, cnt * row_f * 4, cudaMemcpyDeviceToHost, p->sx));
+            ok(cudaMemcpyAsync(h_out + r0 * row_f, sl.out + r0 * row_f, cnt * row_f * 4, cudaMemcpyDeviceToHost, p->sx));
             d2h += cnt * row_f * 4;
         }
         if (h_med && d.full) {
-            ok(cudaMemcpyAsync(h_med + r0 * row_m, p->med + r0 * row_m, cnt * row_m * 4, cudaMemcpyDeviceToHost, p->sx));
+            ok(cudaMemcpyAsync(h_med + r0 * row_m, sl.med + r0 * row_m, cnt * row_m * 4, cudaMemcpyDeviceToHost, p->sx));
             d2h += cnt * row_m * 4;
         }
     };
     if (B == 1) {
-        // 1. image in (straight into the texture array when the sampler reads only the texture)
+        // 1. image in on the upload stream (straight into the texture array when the sampler reads it)
         if (tex)
-            ok(cudaMemcpy2DToArrayAsync(p->arr, 0, 0, h_img, std::size_t(n) * 4, std::size_t(n) * 4, std::size_t(n),
-                                        cudaMemcpyHostToDevice, p->sc[0]));
+            ok(cudaMemcpy2DToArrayAsync(sl.arr, 0, 0, h_img, std::size_t(n) * 4, std::size_t(n) * 4, std::size_t(n),
+                                        cudaMemcpyHostToDevice, p->si));
         else
-            ok(cudaMemcpyAsync(p->img, h_img, N2 * 4, cudaMemcpyHostToDevice, p->sc[0]));
+            ok(cudaMemcpyAsync(sl.img, h_img, N2 * 4, cudaMemcpyHostToDevice, p->si));
         h2d += N2 * 4;
-        ok(cudaEventRecord(p->ready, p->sc[0]));
-        ok(cudaStreamWaitEvent(p->sc[1], p->ready, 0));
+        ok(cudaEventRecord(sl.ready, p->si));
+        ok(cudaStreamWaitEvent(p->sc[0], sl.ready, 0));
+        ok(cudaStreamWaitEvent(p->sc[1], sl.ready, 0));
         // 2. angle chunks alternating over two compute streams; each finished chunk's forward and
         //    mirror rows go out on the copy stream while later chunks compute
         for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
@@ -409,36 +435,34 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
             tt::TraceArgs ta = trace_args(u0, u1, 0, 1);
             if (!ok(tt::launch_trace(ta, s))) break;
             launches += tt::trace_launch_count(ta);
-            ok(cudaEventRecord(p->done[c], s));
-            if (h_out || h_med) {
-                ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
+            ok(cudaEventRecord(sl.done[c], s));
+            ok(cudaStreamWaitEvent(p->sx, sl.done[c], 0));
+            if (h_out || h_med)
                 for (int half = 0; half < (p->pair ? 2 : 1); ++half) download(std::size_t(u0 + half * p->units), u1 - u0);
-            }
         }
-        for (int c = 0; c < p->chunks; ++c) ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
         if (d.features) {  // 3. P-functionals over the whole sinogram
             const std::size_t rows = d.a_count;
-            ok(tt::launch_circus(p->out, n, int(rows * tt::kNumF), p->circ, p->sx));
+            ok(tt::launch_circus(sl.out, n, int(rows * tt::kNumF), sl.circ, p->sx));
             ++launches;
             if (h_circ) {
-                ok(cudaMemcpyAsync(h_circ, p->circ, rows * row_c * 4, cudaMemcpyDeviceToHost, p->sx));
+                ok(cudaMemcpyAsync(h_circ, sl.circ, rows * row_c * 4, cudaMemcpyDeviceToHost, p->sx));
                 d2h += rows * row_c * 4;
             }
         }
     } else {
-        // Image chunks: chunk c's upload (copy-in stream) overlaps chunk c-1's trace + features
-        // (compute stream) and chunk c-2's download (copy-out stream).
+        // Image chunks: chunk c's upload (upload stream) overlaps chunk c-1's atlas fill + trace +
+        // features (compute stream) and chunk c-2's download (copy stream).
         const int units_all = d.a_count;  // rows per image
         for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
             const int b0 = int((long long)B * c / p->chunks), b1 = int((long long)B * (c + 1) / p->chunks);
             const std::size_t cnt = std::size_t(b1 - b0);
-            ok(cudaMemcpyAsync(p->img + b0 * N2, h_img + b0 * N2, cnt * N2 * 4, cudaMemcpyHostToDevice, p->si));
+            ok(cudaMemcpyAsync(sl.img + b0 * N2, h_img + b0 * N2, cnt * N2 * 4, cudaMemcpyHostToDevice, p->si));
             h2d += cnt * N2 * 4;
-            ok(cudaEventRecord(p->uploaded[c], p->si));
+            ok(cudaEventRecord(sl.uploaded[c], p->si));
             cudaStream_t s = p->sc[0];
-            ok(cudaStreamWaitEvent(s, p->uploaded[c], 0));
+            ok(cudaStreamWaitEvent(s, sl.uploaded[c], 0));
             if (tex) {
-                ok(tt::fill_image_atlas(p->arr, p->img + b0 * N2, n, int(cnt), (long long)N2, p->cols, s, b0));
+                ok(tt::fill_image_atlas(sl.arr, sl.img + b0 * N2, n, int(cnt), (long long)N2, p->cols, s, b0));
                 ++launches;
             }
             tt::TraceArgs ta = trace_args(0, p->units, b0, b1);
@@ -446,28 +470,42 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
             launches += tt::trace_launch_count(ta);
             const std::size_t r0 = std::size_t(b0) * units_all, rows = cnt * units_all;
             if (d.features) {
-                ok(tt::launch_circus(p->out + r0 * row_f, n, int(rows * tt::kNumF), p->circ + r0 * row_c, s));
+                ok(tt::launch_circus(sl.out + r0 * row_f, n, int(rows * tt::kNumF), sl.circ + r0 * row_c, s));
                 ++launches;
             }
-            ok(cudaEventRecord(p->done[c], s));
-            ok(cudaStreamWaitEvent(p->sx, p->done[c], 0));
+            ok(cudaEventRecord(sl.done[c], s));
+            ok(cudaStreamWaitEvent(p->sx, sl.done[c], 0));
             download(r0, rows);
             if (d.features && h_circ) {
-                ok(cudaMemcpyAsync(h_circ + r0 * row_c, p->circ + r0 * row_c, rows * row_c * 4, cudaMemcpyDeviceToHost,
+                ok(cudaMemcpyAsync(h_circ + r0 * row_c, sl.circ + r0 * row_c, rows * row_c * 4, cudaMemcpyDeviceToHost,
                                    p->sx));
                 d2h += rows * row_c * 4;
             }
         }
     }
-    ok(cudaStreamSynchronize(p->sx));
-    ok(cudaStreamSynchronize(p->si));
-    ok(cudaStreamSynchronize(p->sc[0]));
-    ok(cudaStreamSynchronize(p->sc[1]));
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "plan run");
+    ok(cudaEventRecord(sl.free, p->sx));  // every download (and, before them, every kernel) of the slot
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "plan submit");
     ctx->c.bytes_h2d += h2d;
     ctx->c.bytes_d2h += d2h;
     ctx->c.gpu_kernel_launches += launches;
     return TT_OK;
+}
+
+tt_status tt_plan_wait(tt_plan* p) {
+    if (!p) return fail(nullptr, TT_ERR_INVALID, "null plan");
+    DeviceGuard guard(p->ctx->device);
+    cudaError_t e = cudaSuccess;
+    for (cudaStream_t s : {p->sx, p->si, p->sc[0], p->sc[1]}) {
+        const cudaError_t x = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) e = x;
+    }
+    return e == cudaSuccess ? TT_OK : cuda_fail(p->ctx, e, "plan wait");
+}
+
+tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t* h_med, float* h_circ) {
+    tt_status st = tt_plan_submit(p, h_img, h_out, h_med, h_circ);
+    if (st != TT_OK) return st;
+    return tt_plan_wait(p);
 }
 
 tt_status tt_plan_chunks(const tt_plan* p, int* chunks) {

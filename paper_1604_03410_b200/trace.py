@@ -188,11 +188,12 @@ class Plan:
     Outputs equal one whole launch bit-for-bit."""
 
     def __init__(self, ctx: DeviceContext, n: int, angles: int, full: bool = True, a0: int = 0,
-                 a_count: int | None = None, features: bool = False, batch: int = 1, chunks: int = 0):
+                 a_count: int | None = None, features: bool = False, batch: int = 1, chunks: int = 0,
+                 slots: int = 0):
         self.ctx, self.n, self.full, self.batch = ctx, n, full, batch
         self.a_count = angles - a0 if a_count is None else a_count
         self.features = features and full
-        d = _lib.PlanDesc(n, angles, a0, self.a_count, int(full), int(self.features), batch, chunks)
+        d = _lib.PlanDesc(n, angles, a0, self.a_count, int(full), int(self.features), batch, chunks, slots)
         self._p = C.c_void_p()
         _check(lib.tt_plan_create(ctx._p, C.byref(d), C.byref(self._p)), ctx._p)
         c = C.c_int()
@@ -200,6 +201,16 @@ class Plan:
         self.chunks = c.value
 
     def run(self, img, out=None, med=None, circ=None) -> None:
+        """Synchronous: returns with the host outputs filled."""
+        self.submit(img, out, med, circ)
+        self.wait()
+
+    def wait(self) -> None:
+        """Drain every submission (tt_plan_wait)."""
+        _check(lib.tt_plan_wait(self._p), self.ctx._p)
+
+    def submit(self, img, out=None, med=None, circ=None) -> None:
+        """Asynchronous (tt_plan_submit): the arrays must stay alive and untouched until wait()."""
         def ptr(a, dt):
             if a is None:
                 return None
@@ -210,7 +221,7 @@ class Plan:
         for a, size in ((out, lead * F * self.n), (med, lead * 2 * self.n), (circ, lead * NF * 3)):
             assert a is None or a.size == size, "output array has the wrong size"
         assert img.size == self.batch * self.n * self.n
-        _check(lib.tt_plan_run(self._p, ptr(img, np.float32), ptr(out, np.float32),
+        _check(lib.tt_plan_submit(self._p, ptr(img, np.float32), ptr(out, np.float32),
                                ptr(med if self.full else None, np.int32), ptr(circ if self.features else None,
                                                                                 np.float32)), self.ctx._p)
 

@@ -91,3 +91,23 @@ def test_plan_rejects_bad_descriptors(ctx):
         tt.Plan(ctx, 64, 10, a0=5, a_count=10)
     with pytest.raises(Exception):
         tt.Plan(ctx, 64, 0)
+
+
+@pytest.mark.parametrize("slots", [1, 2, 3])
+def test_overlapping_submissions_equal_separate_runs(ctx, slots):
+    n, A = 256, 48
+    imgs = [tt.synth_image(k, n) for k in (tt.DISK, tt.PHANTOM, tt.SPARSE, tt.DISK)]
+    plan = tt.Plan(ctx, n, A, features=True, chunks=3, slots=slots)
+    refs = []
+    for img in imgs:
+        o, m, c = np.empty((A, NF, n), np.float32), np.empty((A, 2, n), np.int32), np.empty((A, NF, 3), np.float32)
+        plan.run(img, o, m, c)
+        refs.append((o, m, c))
+    outs = [(np.full((A, NF, n), np.nan, np.float32), np.zeros((A, 2, n), np.int32), np.zeros((A, NF, 3), np.float32))
+            for _ in imgs]
+    for img, (o, m, c) in zip(imgs, outs):
+        plan.submit(img, o, m, c)
+    plan.wait()
+    for (o, m, c), (ro, rm, rc) in zip(outs, refs):
+        assert np.array_equal(_bits(o), _bits(ro)) and np.array_equal(m, rm) and np.array_equal(_bits(c), _bits(rc))
+    plan.destroy()
