@@ -10,6 +10,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <iostream>
 #include <limits>
 #include <string>
@@ -147,7 +149,25 @@ std::vector<float> ramp(int n, float a, float b) {
 
 }  // namespace
 
-int main() {
+// --trace-vptx <krn>: the VPTX the reference front end produces for the trace
+// kernel's launch signature trace_t05(f32[], i32, f32[], f32[], f32[], f32[], i32[], i32).
+int print_trace_vptx(const char* path) {
+    std::ifstream f(path);
+    std::stringstream ss;
+    ss << f.rdbuf();
+    KernelAst ast = parse_kernel(ss.str());
+    std::vector<float> fv(1);
+    std::vector<std::int32_t> iv(1);
+    std::vector<KernelArg> args = {cu_in(fv), std::int32_t(0), cu_in(fv), cu_in(fv), cu_in(fv),
+                                   cu_out(fv), cu_out(iv), std::int32_t(0)};
+    std::vector<ArgType> types;
+    for (const auto& a : args) types.push_back(a.arg_type());
+    std::cout << disassemble(lower(specialize(ast, types)));
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc == 3 && std::string(argv[1]) == "--trace-vptx") return print_trace_vptx(argv[2]);
     std::vector<Case> cases;
     const float nan = std::numeric_limits<float>::quiet_NaN(), inf = std::numeric_limits<float>::infinity();
     {  // the reference's sample kernels (proj/kernels/*.krn)

@@ -100,3 +100,42 @@ def test_jit_rejects_invalid_bodies_with_validation_failed(ctx):
     mh = ctx.module_load(bad)
     with pytest.raises(tt.ValidationFailed):
         ctx.get_function(mh, "k")
+
+
+TRACE_VPTX = open(os.path.join(os.path.dirname(__file__), "golden", "trace_t05.vptx")).read()
+
+
+def _run_dsl_trace(ctx, img, n, A, c, s, w, block=64):
+    """oracle/trace_t05.krn as the reference front end compiles it, run through the JIT
+    (renamed so the native fused kernel does not replace it)."""
+    mh = ctx.module_load(TRACE_VPTX.replace(".kernel trace_t05(", ".kernel trace_t05_dsl(", 1))
+    fn = ctx.get_function(mh, "trace_t05_dsl")
+    bufs = [ctx.mem_alloc(x.nbytes) for x in (img, c, s, w)]
+    for b, x in zip(bufs, (img, c, s, w)):
+        ctx.memcpy_htod(b, np.ascontiguousarray(x))
+    out_d, med_d = ctx.mem_alloc(A * 6 * n * 4), ctx.mem_alloc(A * 2 * n * 4)
+    res = ctx.launch(fn, tt.GridConfig((A, (n + block - 1) // block, 1), (block, 1, 1)),
+                     [bufs[0], np.int32(n), bufs[1], bufs[2], bufs[3], out_d, med_d, np.int32(0)])
+    out = np.empty((A, 6, n), np.float32)
+    med = np.empty((A, 2, n), np.int32)
+    ctx.memcpy_dtoh(out, out_d)
+    ctx.memcpy_dtoh(med, med_d)
+    for b in bufs + [out_d, med_d]:
+        ctx.mem_free(b)
+    return res, out, med
+
+
+@pytest.mark.parametrize("n,A,kind", [(32, 6, tt.DISK), (64, 10, tt.PHANTOM), (100, 7, tt.SPARSE)])
+def test_jit_of_the_reference_dsl_trace_kernel_equals_seq32_oracle(ctx, n, A, kind):
+    """The trace transform written in the reference DSL, compiled by the reference front end and
+    run through the JIT, equals the oracle's SEQ32 mode (= the reference emulator, tier 2)
+    bit-for-bit: the JIT, the oracle and the emulator agree on every bit of the path."""
+    import oracle as O
+
+    img = tt.synth_image(kind, n)
+    c, s, w = tt.make_tables(n, A)
+    res, out, med = _run_dsl_trace(ctx, img, n, A, c, s, w)
+    assert res.ok(), res.trap
+    rout, rmed, _, _ = O.transform(img, n, c, s, w, mode=O.SEQ32)
+    assert np.array_equal(out.view(np.uint32), rout.view(np.uint32))
+    assert np.array_equal(med, rmed)
