@@ -124,14 +124,21 @@ def fp32_peak_tflops(torch, tt, stream) -> float:
 
 
 def load_traffic(workload: str):
-    """dram bytes per launch of the fused kernel from the committed ncu summary."""
+    """dram bytes per launch of the fused kernel (and its pipe utilisations) from the committed ncu summary."""
     p = os.path.join(ROOT, "profiles", f"ncu_{workload}_summary.json")
     try:
         with open(p) as f:
             j = json.load(f)
-        return j.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT)
     except Exception:
-        return None, None
+        return None, None, None
+    pipes = None
+    if "issue_slots_busy_pct" in j:
+        # north_star: "SM FP32 and shared-memory pipe utilisation" for L2-resident images
+        pipes = {"issue_slots_busy": j["issue_slots_busy_pct"] / 100.0,
+                 "l1tex_shared_throughput": j.get("l1tex_throughput_pct", 0.0) / 100.0,
+                 "fma_pipe_cycles_active": j.get("fma_pipe_active_pct", 0.0) / 100.0 or None,
+                 "source": os.path.relpath(p, ROOT) + " (ncu --set full of one launch)"}
+    return j.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT), pipes
 
 
 def cpu_baseline(wl, seconds_target=10.0):
@@ -400,7 +407,7 @@ def run_ours(args, ws, rank, local):
     kern_s = statistics.mean(kern_ms) / 1e3
     peak = fp32_peak_tflops(torch, tt, stream)
     achieved = FLOPS_PER_TAP[full] * taps / kern_s / 1e12
-    traffic, traffic_src = load_traffic(args.workload)
+    traffic, traffic_src, pipes = load_traffic(args.workload)
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic,
                 "peak_source": "measured in this run: tt_ffma_probe (8 independent FFMA chains x 148*8 CTAs), "
@@ -409,6 +416,8 @@ def run_ours(args, ws, rank, local):
                 "kernel_ms": kern_s * 1e3, "taps_per_s": taps / kern_s,
                 "hbm_algorithmic_bytes": B * (n * n * 4 + a_cnt * (F + 2) * n * 4),
                 "traffic_source": traffic_src}
+    if pipes:
+        roofline["ncu_pipes"] = pipes
     scaling = "strong" if (orient or images) else "weak"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
