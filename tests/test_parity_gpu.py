@@ -261,6 +261,20 @@ def test_tiny_and_denormal_values_exact(ctx):
         assert _bitwise_equal(out, rout) and np.array_equal(med, rmed)
 
 
+@pytest.mark.parametrize("n,A", [(256, 6), (1024, 4), (2048, 2)])
+def test_mixed_magnitude_values_exact(ctx, n, A):
+    """Pixels spanning denormals to 1e25 in one image: tap pairs whose square roots take
+    different (scaled / unscaled) paths inside one packed sqrt2_rn, on each schedule."""
+    rng = np.random.default_rng(n)
+    expo = rng.uniform(-44.0, 25.0, size=(n, n))
+    img = (tt.synth_image(tt.DISK, n).astype(np.float64) * 10.0 ** expo).astype(np.float32)
+    img[rng.random((n, n)) < 0.05] = 0.0
+    tr, out, med = _run(ctx, img, n, A, sampler=1)
+    ctx.set_sampler(0)
+    rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY)
+    assert _bitwise_equal(out, rout) and np.array_equal(med, rmed)
+
+
 @pytest.mark.parametrize("n,A", [(256, 12), (1000, 6), (1024, 8)])
 def test_prepared_weight_layout_equals_per_call_conversion(ctx, n, A):
     """tt_weights_soa + tt_trace_desc.wsoa gives the same bits as the per-call conversion."""
