@@ -297,6 +297,15 @@ tt_status tt_ipc_close(void* d_ptr);
  * median, max).  For a trace output [a][6][n], rows = 6a. */
 tt_status tt_circus_device(const float* d_sino, int n, int rows, float* d_circ, void* stream);
 
+/* Spectral P-functional (the optional |FFT|^4 functional of the
+ * paper's circus stage) of `rows` sinogram rows of length n (1 <= n <= 16384) on
+ * device: d_p[row] = sum_k |F(s)_k|^4 (double: the 4th powers of T1/T2 rows exceed
+ * the f32 range), F the length-n DFT of the row.  fp32 FFT (power-of-two n) or
+ * direct DFT, f64 accumulation of the powers; rtol 1e-4
+ * against an f64 FFT.  No reference interface exists for it (the reference has
+ * no trace-transform code); it sits beside tt_circus_device. */
+tt_status tt_circus_fft_device(const float* d_sino, int n, int rows, double* d_p, void* stream);
+
 /* Prepared texture for repeated tt_trace_device calls on one image
  * (sampler 1 without the per-call copy). */
 typedef struct tt_image_tex tt_image_tex;

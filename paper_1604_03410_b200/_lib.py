@@ -1,5 +1,5 @@
 """ctypes binding of include/tt_b200.h.  Raises at import if libtt_b200.so
-is missing (build it with ``python -m paper_1604_03410_b200.build`` or
+is missing (build it with ``python paper_1604_03410_b200/build.py`` or
 ``__graft_entry__.build()``) — there is deliberately no fallback."""
 from __future__ import annotations
 
@@ -9,7 +9,7 @@ import os
 LIB_PATH = os.environ.get("TT_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtt_b200.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1604_03410_b200.build` "
+    raise ImportError(f"{LIB_PATH} not built: run `python paper_1604_03410_b200/build.py` "
                       "(the trace transform has no CPU fallback)")
 
 
@@ -114,6 +114,7 @@ _sigs = {
     "tt_ipc_import": (_S, [C.POINTER(IpcHandle), C.c_int, C.POINTER(C.c_void_p)]),
     "tt_ipc_close": (_S, [C.c_void_p]),
     "tt_circus_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "tt_circus_fft_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_image_tex_create": (_S, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     "tt_image_atlas_create": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p)]),
     "tt_image_tex_update": (_S, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),

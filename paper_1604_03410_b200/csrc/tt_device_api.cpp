@@ -147,6 +147,13 @@ tt_status tt_circus_device(const float* d_sino, int n, int rows, float* d_circ, 
     return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "circus");
 }
 
+tt_status tt_circus_fft_device(const float* d_sino, int n, int rows, double* d_p, void* stream) {
+    if (!d_sino || !d_p || n < 1 || n > tt::max_circus_fft_n() || rows < 0)
+        return fail(nullptr, TT_ERR_INVALID, "bad circus_fft arguments");
+    cudaError_t e = tt::launch_circus_fft(d_sino, n, rows, d_p, (cudaStream_t)stream);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "circus_fft");
+}
+
 tt_status tt_image_tex_create(const float* d_img, int n, void* stream, tt_image_tex** out) {
     if (!d_img || !out || n < 1) return fail(nullptr, TT_ERR_INVALID, "bad argument");
     auto t = std::make_unique<tt_image_tex>();

@@ -104,6 +104,9 @@ cudaError_t launch_ffma_probe(float* out, int blocks, int iters, cudaStream_t s)
 // circ[row][3] = (P1 total variation, P2 weighted-median value, P3 max),
 // DESIGN.md §2.7.  One warp per row.
 cudaError_t launch_circus(const float* sino, int n, int rows, float* circ, cudaStream_t s);
+// Spectral P-functional sum_k |F(s)_k|^4 of each row, n <= max_circus_fft_n().
+cudaError_t launch_circus_fft(const float* sino, int n, int rows, double* pout, cudaStream_t s);
+int max_circus_fft_n();
 
 // Texture atlas of `batch` images (image b at tile (b % cols, b / cols)),
 // 32-bit texels holding the float bits.

@@ -304,6 +304,11 @@ def circus_device(sino_ptr: int, n: int, rows: int, circ_ptr: int, stream: int =
     _check(lib.tt_circus_device(C.c_void_p(sino_ptr), n, rows, C.c_void_p(circ_ptr), C.c_void_p(stream)))
 
 
+def circus_fft_device(sino_ptr: int, n: int, rows: int, p_ptr: int, stream: int = 0) -> None:
+    """Spectral P-functional sum_k |F(s)_k|^4 of `rows` device sinogram rows (tt_circus_fft_device)."""
+    _check(lib.tt_circus_fft_device(C.c_void_p(sino_ptr), n, rows, C.c_void_p(p_ptr), C.c_void_p(stream)))
+
+
 def circus(ctx: DeviceContext, sino: np.ndarray):
     """P-functionals of host sinogram rows through cuda_launch (circus kernel)."""
     sino = np.ascontiguousarray(sino, np.float32)
