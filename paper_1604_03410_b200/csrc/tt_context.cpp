@@ -482,6 +482,27 @@ LaunchOutcome run_circus(tt_ctx& ctx, const tt_grid&, const std::vector<Resolved
     return o;
 }
 
+// circus_fft(sino, n, rows, pf): the spectral P-functional sum_k |F(s)_k|^4 of
+// each row -> pf[rows] (f64).
+LaunchOutcome run_circus_fft(tt_ctx& ctx, const tt_grid&, const std::vector<ResolvedArg>& a) {
+    LaunchOutcome o;
+    const int n = a[1].value.v.i32, rows = a[2].value.v.i32;
+    if (n <= 0 || rows <= 0) return o;
+    if (n > tt::max_circus_fft_n()) {
+        o.status = TT_ERR_LAUNCH_CONFIG;
+        o.error = "LaunchConfigError: circus_fft row length above 16384";
+        return o;
+    }
+    if (elems(a[0], 4) < std::uint64_t(n) * std::uint64_t(rows) || elems(a[3], 8) < std::uint64_t(rows)) {
+        o.trap = first_thread_trap(TT_TRAP_GLOBAL_OUT_OF_BOUNDS);
+        return o;
+    }
+    o = cuda_outcome(tt::launch_circus_fft((const float*)a[0].dptr, n, rows, (double*)a[3].dptr, ctx.stream),
+                     "circus_fft");
+    o.gpu_launches = 1;
+    return o;
+}
+
 Param P(bool ptr, Scalar t, const char* name, bool written = false) {
     Param p;
     p.ptr = ptr;
@@ -500,7 +521,8 @@ const std::vector<NativeKernel>& registry() {
             nk.decl.params = std::move(ps);
             nk.fn = fn;
             const std::string nm = name;
-            nk.replaces_body = nm == "trace_t05" || nm == "trace_t05_batch" || nm == "radon" || nm == "circus";
+            nk.replaces_body = nm == "trace_t05" || nm == "trace_t05_batch" || nm == "radon" || nm == "circus" ||
+                               nm == "circus_fft";
             r.push_back(std::move(nk));
         };
         const Scalar f = Scalar::F32, d = Scalar::F64, i = Scalar::I32, l = Scalar::I64;
@@ -518,6 +540,8 @@ const std::vector<NativeKernel>& registry() {
             run_radon);
         add("circus", {P(true, f, "sino"), P(false, i, "n"), P(false, i, "rows"), P(true, f, "circ", true)},
             run_circus);
+        add("circus_fft", {P(true, f, "sino"), P(false, i, "n"), P(false, i, "rows"), P(true, d, "pf", true)},
+            run_circus_fft);
         add("vadd", {P(true, f, "a"), P(true, f, "b"), P(true, f, "c", true)}, run_vadd<tt::ElemKind::F32, 4>);
         add("vadd", {P(true, d, "a"), P(true, d, "b"), P(true, d, "c", true)}, run_vadd<tt::ElemKind::F64, 8>);
         add("vadd", {P(true, i, "a"), P(true, i, "b"), P(true, i, "c", true)}, run_vadd<tt::ElemKind::I32, 4>);

@@ -23,6 +23,7 @@ NF = 6
 
 TRACE_T05 = KernelAst("trace_t05", ["img", "n", "ctab", "stab", "wtab", "out", "med", "a0"])
 CIRCUS = KernelAst("circus", ["sino", "n", "rows", "circ"])
+CIRCUS_FFT = KernelAst("circus_fft", ["sino", "n", "rows", "pf"])
 TRACE_T05_BATCH = KernelAst("trace_t05_batch", ["img", "n", "ctab", "stab", "wtab", "out", "med", "a0", "batch"])
 RADON = KernelAst("radon", ["img", "n", "ctab", "stab", "out", "a0"])
 
@@ -320,6 +321,19 @@ def circus(ctx: DeviceContext, sino: np.ndarray):
     if not rep.ok():
         raise RuntimeError(f"circus launch trapped: {rep.trap}")
     return circ
+
+
+def circus_fft(ctx: DeviceContext, sino: np.ndarray):
+    """Spectral P-functional sum_k |F(s)_k|^4 of host sinogram rows through cuda_launch (f64 per row)."""
+    sino = np.ascontiguousarray(sino, np.float32)
+    n = sino.shape[-1]
+    rows = sino.size // n
+    pf = np.empty(sino.shape[:-1], np.float64)
+    rep = cuda_launch(ctx, CIRCUS_FFT, GridConfig((rows, 1, 1), (256, 1, 1)),
+                      [cu_in(sino), np.int32(n), np.int32(rows), cu_out(pf)])
+    if not rep.ok():
+        raise RuntimeError(f"circus_fft launch trapped: {rep.trap}")
+    return pf
 
 
 def image_texture(img_ptr: int, n: int, stream: int = 0):

@@ -63,3 +63,12 @@ def test_pfft_rejects_bad_arguments(ctx):
     with pytest.raises(Exception):
         tt.circus_fft_device(p, 16385, 1, p, ctx.stream)
     tt.circus_fft_device(p, 16, 0, p, ctx.stream)  # no rows: no work
+
+
+def test_pfft_through_cuda_launch_equals_device_entry(ctx):
+    """The module path (cuda_launch of a `circus_fft(f32[],i32,i32,f64[])` kernel, bound natively)
+    gives the same bits as tt_circus_fft_device."""
+    rows = np.random.default_rng(5).random((2, 6, 512)).astype(np.float32)
+    via_launch = tt.circus_fft(ctx, rows)
+    assert via_launch.shape == (2, 6)
+    assert np.array_equal(via_launch.reshape(-1), _gpu_pfft(ctx, rows.reshape(-1, 512)))
