@@ -337,9 +337,11 @@ struct Translator {
             if (!R(l.no, ld ? ops[1] : ops[0], Ty::I64, addr) || !R(l.no, ld ? ops[0] : ops[1], t, data)) return false;
             const std::string nb = std::to_string(ty_bytes(t));
             if (p[1] == "global") {
-                body << "  { const unsigned long long a_ = (unsigned long long)" << addr
-                     << "; const int c_ = tt_gcheck(tt_rng, tt_nrng, a_, " << nb
-                     << "); if (c_ != 2) TT_TRAP(c_ == 1 ? 2 : 0, " << I << ", 0); ";
+                // one-entry per-thread cache of the last live allocation hit (the table is
+                // fixed for the launch): the binary search runs only on a miss
+                body << "  { const unsigned long long a_ = (unsigned long long)" << addr << "; if (!(a_ >= tt_clo && a_ + "
+                     << nb << "ull <= tt_chi && a_ + " << nb << "ull >= a_)) { const int c_ = tt_gcheck(tt_rng, tt_nrng, a_, "
+                     << nb << ", tt_clo, tt_chi); if (c_ != 2) TT_TRAP(c_ == 1 ? 2 : 0, " << I << ", 0); } ";
                 if (ld) body << data << " = tt_ld<" << cty(t) << ">((const unsigned char*)a_); }\n";
                 else body << "tt_st<" << cty(t) << ">((unsigned char*)a_, " << data << "); }\n";
             } else {
@@ -408,11 +410,13 @@ struct Translator {
              "  atomicExch(&t->lock, 0);\n"
              "}\n"
              "// 0: outside every allocation, 1: inside a freed one, 2: live (rng: sorted [begin, end, live])\n"
-             "__device__ __forceinline__ int tt_gcheck(const u64* rng, int nr, u64 a, unsigned len) {\n"
+             "__device__ __forceinline__ int tt_gcheck(const u64* rng, int nr, u64 a, unsigned len, u64& clo, u64& chi) {\n"
              "  int lo = 0, hi = nr - 1, f = -1;\n"
              "  while (lo <= hi) { const int m = (lo + hi) >> 1; if (rng[3 * m] <= a) { f = m; lo = m + 1; } else hi = m - 1; }\n"
              "  if (f < 0 || a + len > rng[3 * f + 1] || a + len < a) return 0;\n"
-             "  return rng[3 * f + 2] ? 2 : 1;\n"
+             "  if (!rng[3 * f + 2]) return 1;\n"
+             "  clo = rng[3 * f]; chi = rng[3 * f + 1];\n"
+             "  return 2;\n"
              "}\n"
              "template <class T> __device__ __forceinline__ T tt_ld(const unsigned char* p) {\n"
              "  if (((u64)p & (sizeof(T) - 1)) == 0) return *(const T*)p;\n"
@@ -429,6 +433,7 @@ struct Translator {
         s << "TtTrap* tt_trap, const u64* tt_rng, int tt_nrng, unsigned tt_shbytes) {\n"
              "  extern __shared__ __align__(16) unsigned char tt_sh[];\n"
              "  unsigned tt_phase = 0;\n"
+             "  u64 tt_clo = 1, tt_chi = 0;  // cached live allocation [lo, hi): empty\n"
           << decl.str() << body.str()
           << "  return;\n"  // control never falls off the end of a valid body
              "}\n";
