@@ -215,13 +215,18 @@ class Plan:
         def ptr(a, dt):
             if a is None:
                 return None
-            assert a.dtype == dt and a.flags["C_CONTIGUOUS"]
+            if a.dtype != dt or not a.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"plan arrays must be C-contiguous {np.dtype(dt).name}")
             return C.c_void_p(a.ctypes.data)
+        if not self._p:
+            raise ValueError("plan destroyed")
         F = NF if self.full else 1
         lead = self.batch * self.a_count
         for a, size in ((out, lead * F * self.n), (med, lead * 2 * self.n), (circ, lead * NF * 3)):
-            assert a is None or a.size == size, "output array has the wrong size"
-        assert img.size == self.batch * self.n * self.n
+            if a is not None and a.size != size:
+                raise ValueError(f"output array has {a.size} elements, the plan writes {size}")
+        if img.size != self.batch * self.n * self.n:
+            raise ValueError(f"image array has {img.size} elements, the plan reads {self.batch * self.n * self.n}")
         _check(lib.tt_plan_submit(self._p, ptr(img, np.float32), ptr(out, np.float32),
                                ptr(med if self.full else None, np.int32), ptr(circ if self.features else None,
                                                                                 np.float32)), self.ctx._p)
@@ -230,6 +235,12 @@ class Plan:
         if self._p:
             lib.tt_plan_destroy(self._p)
             self._p = C.c_void_p()
+
+    def __enter__(self) -> "Plan":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.destroy()
 
 
 def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, stab_ptr: int, wtab_ptr: int,

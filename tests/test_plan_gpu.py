@@ -93,6 +93,23 @@ def test_plan_rejects_bad_descriptors(ctx):
         tt.Plan(ctx, 64, 0)
 
 
+def test_plan_validates_host_arrays_and_closes(ctx):
+    n, A = 64, 8
+    img = tt.synth_image(tt.DISK, n)
+    with tt.Plan(ctx, n, A) as plan:
+        with pytest.raises(ValueError):
+            plan.run(img, np.empty((A, NF, n - 1), np.float32))       # wrong size
+        with pytest.raises(ValueError):
+            plan.run(img, np.empty((A, NF, n), np.float64))           # wrong dtype
+        with pytest.raises(ValueError):
+            plan.run(img[:, :-1].copy())                              # wrong image size
+        out = np.empty((A, NF, n), np.float32)
+        plan.run(img, out)
+    assert not plan._p
+    with pytest.raises(ValueError):
+        plan.run(img, out)                                            # destroyed
+
+
 @pytest.mark.parametrize("slots", [1, 2, 3])
 def test_overlapping_submissions_equal_separate_runs(ctx, slots):
     n, A = 256, 48
