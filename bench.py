@@ -333,7 +333,8 @@ def run_ours(args, ws, rank, local):
     nbs = (nb_img, nb_out if want_sino else 4, nb_med if want_sino else 4, nb_circ)
     hp = [C.c_void_p() for _ in range(7)]
     for hh, nb in zip(hp, nbs + nbs[1:]):
-        assert lib.tt_host_alloc(nb, C.byref(hh)) == 0
+        if lib.tt_host_alloc(nb, C.byref(hh)) != 0:
+            raise RuntimeError(f"tt_host_alloc({nb}) failed")
     h_img = np.ctypeslib.as_array((C.c_float * (B * n * n)).from_address(hp[0].value)).reshape(img_h.shape)
     h_img[:] = img_h
     outs = []
