@@ -123,6 +123,25 @@ def fp32_peak_tflops(torch, tt, stream) -> float:
     return flops / best / 1e12
 
 
+def tex_peak_gathers(torch, stream) -> float:
+    """Measured texture-gather throughput (TLD4 lane-gathers/s, L1-resident texture) of this GPU:
+    the roofline of the sampling stage (one gather per sampled tap)."""
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    blocks, iters = props.multi_processor_count * 8, 1024
+    buf = torch.empty(blocks, dtype=torch.int32, device="cuda")
+    from paper_1604_03410_b200._lib import lib
+    lib.tt_tld4_probe(buf.data_ptr(), blocks, 16, stream.cuda_stream)
+    best = float("inf")
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lib.tt_tld4_probe(buf.data_ptr(), blocks, iters, stream.cuda_stream)
+        e1.record(stream)
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    return blocks * 256.0 * iters * 8 / best
+
+
 def load_traffic(workload: str):
     """dram bytes per launch of the fused kernel (and its pipe utilisations) from the committed ncu summary."""
     p = os.path.join(ROOT, "profiles", f"ncu_{workload}_summary.json")
@@ -419,6 +438,15 @@ def run_ours(args, ws, rank, local):
                 "traffic_source": traffic_src}
     if pipes:
         roofline["ncu_pipes"] = pipes
+    # the sampling stage's own roofline: one TLD4 lane-gather per sampled tap; mirrored angle pairs
+    # share one sampling pass, so a launch issues B * (a_cnt / 2) * n^2 gathers (in- and out-of-range)
+    if tex is not None:
+        gpk = B * (a_cnt // 2) * n * n
+        tpeak = tex_peak_gathers(torch, stream)
+        roofline["tex_gather"] = {"achieved": gpk / kern_s, "peak": tpeak, "unit": "gathers/s",
+                                  "frac": gpk / kern_s / tpeak, "gathers_per_launch": gpk,
+                                  "peak_source": "measured in this run: tt_tld4_probe (8 independent TLD4 per "
+                                                 "thread, L1-resident texture, 148*8 CTAs)"}
     scaling = "strong" if (orient or images) else "weak"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

@@ -233,6 +233,9 @@ tt_status tt_pgm_write(const char* path, const float* img, int h, int w, float l
 /* FP32 roofline probe: enqueue blocks x 256 threads x iters x 128 FFMA on
  * `stream` (2 flop each); out needs `blocks` floats of device memory. */
 tt_status tt_ffma_probe(float* d_out, int blocks, int iters, void* stream);
+/* Texture-gather roofline probe: blocks x 256 threads x iters x 8 TLD4 gathers
+ * (one lane-gather each) on an L1-resident texture; out needs `blocks` uints. */
+tt_status tt_tld4_probe(unsigned* d_out, int blocks, int iters, void* stream);
 
 /* Raw device-pointer entry (multi-GPU driver, benchmarks): enqueue the fused
  * kernel for a_count angles on `stream` (cudaStream_t; NULL = legacy

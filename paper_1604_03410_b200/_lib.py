@@ -108,6 +108,7 @@ _sigs = {
                          C.c_size_t]),
     "tt_pgm_write": (_S, [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_float]),
     "tt_ffma_probe": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "tt_tld4_probe": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "tt_trace_device": (_S, [C.POINTER(TraceDesc), C.c_void_p]),
     "tt_weights_soa": (_S, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_ipc_export": (_S, [C.c_void_p, C.POINTER(IpcHandle)]),

@@ -26,6 +26,11 @@ tt_status tt_ffma_probe(float* d_out, int blocks, int iters, void* stream) {
     cudaError_t e = tt::launch_ffma_probe(d_out, blocks, iters, (cudaStream_t)stream);
     return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "ffma probe");
 }
+tt_status tt_tld4_probe(unsigned* d_out, int blocks, int iters, void* stream) {
+    if (!d_out || blocks < 1 || iters < 1) return fail(nullptr, TT_ERR_INVALID, "bad probe arguments");
+    cudaError_t e = tt::launch_tld4_probe(d_out, blocks, iters, (cudaStream_t)stream);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "tld4 probe");
+}
 int tt_max_full_n(void) { return tt::max_full_n(); }
 
 static tt_status check_desc(const tt_trace_desc* d) {

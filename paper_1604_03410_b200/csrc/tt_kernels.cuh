@@ -99,6 +99,7 @@ cudaError_t make_image_texture(const float* img, int n, cudaStream_t s, cudaArra
 
 // FP32 roofline probe: blocks x 256 threads x iters x 128 FFMA (2 flop each).
 cudaError_t launch_ffma_probe(float* out, int blocks, int iters, cudaStream_t s);
+cudaError_t launch_tld4_probe(unsigned* out, int blocks, int iters, cudaStream_t s);
 
 // P-functionals (circus features) of `rows` sinogram rows of length n:
 // circ[row][3] = (P1 total variation, P2 weighted-median value, P3 max),

@@ -2,7 +2,7 @@
 180..2880, T0-only (Radon) vs T0-T5, one GPU.  Device-resident timing with
 CUDA events on the launch stream, L2 flushed before every timed launch.
 Prints one JSON line per point (ms, sinogram samples/s, taps/s, FLOP
-fraction of the measured FFMA peak).
+fraction of the measured FFMA peak, fraction of the measured TLD4 gather peak).
 
   python scripts/sweep.py [--quick] > profiles/sweep_rNN.jsonl
 """
@@ -20,7 +20,7 @@ from paper_1604_03410_b200._lib import lib  # noqa: E402
 from paper_1604_03410_b200.trace import image_texture, image_texture_destroy  # noqa: E402
 
 
-def run_point(n, A, full, stream, flush, reps, peak):
+def run_point(n, A, full, stream, flush, reps, peak, tpeak):
     F = 6 if full else 1
     c, s, w = tt.make_tables(n, A)
     img = torch.from_numpy(tt.synth_image(tt.DISK, n)).cuda()
@@ -55,7 +55,9 @@ def run_point(n, A, full, stream, flush, reps, peak):
     flops = bench.FLOPS_PER_TAP[full] * taps
     return {"n": n, "angles": A, "functionals": "T0-T5" if full else "T0", "ms": ms,
             "samples_per_s": F * A * n / (ms / 1e3), "taps_per_s": taps / (ms / 1e3),
-            "tflops": flops / (ms / 1e3) / 1e12, "fp32_frac": flops / (ms / 1e3) / 1e12 / peak}
+            "tflops": flops / (ms / 1e3) / 1e12, "fp32_frac": flops / (ms / 1e3) / 1e12 / peak,
+            # one TLD4 per sampled tap; mirrored angle pairs share a pass (A/2 passes of n^2 taps)
+            "tex_gather_frac": (A // 2) * n * n / (ms / 1e3) / tpeak}
 
 
 def main():
@@ -65,6 +67,7 @@ def main():
     stream = torch.cuda.Stream()
     flush = torch.empty(int(256 << 20) // 4, device="cuda")
     peak = bench.fp32_peak_tflops(torch, tt, stream)
+    tpeak = bench.tex_peak_gathers(torch, stream)
     ns = [128, 256, 512, 1024, 2048, 4096, 8192]
     angles = [180, 360, 720, 1440, 2880]
     if args.quick:
@@ -75,8 +78,9 @@ def main():
                 if full and n > tt.max_full_n():
                     continue
                 reps = 5 if n * n * A > 4e10 else 10
-                pt = run_point(n, A, full, stream, flush, reps, peak)
+                pt = run_point(n, A, full, stream, flush, reps, peak, tpeak)
                 pt["fp32_peak_tflops"] = peak
+                pt["tex_peak_gathers_per_s"] = tpeak
                 print(json.dumps(pt), flush=True)
 
 

@@ -47,6 +47,8 @@ def test_gpu_arm_contract():
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
     assert 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    t = r["tex_gather"]  # the sampling stage's roofline (measured TLD4 peak)
+    assert 0 < t["frac"] < 1 and t["gathers_per_launch"] == 180 * 256 * 256
     assert d["gpu_launches"] == 3  # one fused trace launch per step (C1 has no circus stage)
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
