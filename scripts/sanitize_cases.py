@@ -16,6 +16,7 @@ for sampler in (0, 1):
         out, med, rep = tr(img)
         assert rep.ok()
         tt.circus(ctx, out)
+        tt.circus_fft(ctx, out)
         r = tt.TraceTransform(ctx, n, A, full=False)(img)
     B = 3
     imgs = np.stack([tt.synth_image(tt.DISK, 128, 20160412 + b) for b in range(B)])
