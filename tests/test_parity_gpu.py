@@ -18,7 +18,8 @@ pytestmark = pytest.mark.gpu
 SMALL = [  # (n, A, kind)
     (1, 3, tt.DISK), (2, 4, tt.DISK), (16, 8, tt.DISK), (31, 7, tt.PHANTOM), (33, 5, tt.SPARSE),
     (100, 13, tt.SPARSE), (128, 24, tt.DISK), (255, 9, tt.PHANTOM), (256, 360, tt.DISK),  # C1
-    (300, 20, tt.PHANTOM), (512, 16, tt.SPARSE), (1000, 8, tt.DISK), (1024, 16, tt.PHANTOM),
+    (300, 20, tt.PHANTOM), (512, 16, tt.SPARSE), (1000, 8, tt.DISK), (1001, 6, tt.PHANTOM), (1024, 16, tt.PHANTOM),
+    (2047, 3, tt.SPARSE), (3000, 2, tt.DISK),
     (1536, 5, tt.DISK), (2048, 6, tt.SPARSE), (4096, 3, tt.DISK), (8192, 2, tt.PHANTOM), (16384, 1, tt.DISK),
 ]
 
