@@ -365,10 +365,21 @@ static float chunk_sum(const float* u, int n, int start, int K) {
     return acc;
 }
 
+/* Median chunk length of the kernel (tt_kernels.cu chunk_len): ceil(n/NS),
+ * an even K that is not a power of two rounded up to one; trailing slots may
+ * own short or empty chunks. */
+static int chunk_len(int n, int NS) {
+    const int K = (n + NS - 1) / NS;
+    if ((K & 1) || (K & (K - 1)) == 0) return K;
+    int p = 1;
+    while (p < K) p <<= 1;
+    return p;
+}
+
 /* Weighted median of u under the kernel's schedule. */
 static int replay_median(const float* u, int n, float S, int NS) {
     const int LG = lanes_of(NS);
-    const int K = (n + NS - 1) / NS;
+    const int K = chunk_len(n, NS);
     float E = 0.0f;
     for (int w = 0; w < NS / LG; ++w) {
         float c[32], inc[32];
