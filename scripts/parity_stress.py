@@ -23,16 +23,25 @@ for i in range(count):
     sampler = int(rng.integers(0, 2))
     full = bool(rng.random() < 0.8)
     ctx.set_sampler(sampler)
-    img = tt.synth_image(kind, n, int(rng.integers(0, 1 << 30)))
-    tr = tt.TraceTransform(ctx, n, A, full=full)
-    out, med, rep = tr(img)
-    ref, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY, full=full)
-    ok = rep.ok() and np.array_equal(out.view(np.uint32), ref.view(np.uint32))
-    if full:
-        ok = ok and np.array_equal(med, rmed)
+    # angle sub-ranges (a0, a_count) and image batches (trace_t05_batch) as well
+    a0 = int(rng.integers(0, A)) if rng.random() < 0.2 else 0
+    a_count = int(rng.integers(1, A - a0 + 1)) if a0 else A
+    batch = int(rng.integers(2, 4)) if (full and n <= 1100 and rng.random() < 0.15) else 1
+    imgs = [tt.synth_image(kind, n, int(rng.integers(0, 1 << 30))) for _ in range(batch)]
+    tr = tt.TraceTransform(ctx, n, A, full=full, a0=a0, a_count=a_count, batch=batch)
+    out, med, rep = tr(np.stack(imgs) if batch > 1 else imgs[0])
+    ok = rep.ok()
+    for b, img in enumerate(imgs):
+        ref, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY, full=full, a0=a0,
+                                      a_count=a_count)
+        ob = out[b] if batch > 1 else out
+        ok = ok and np.array_equal(ob.view(np.uint32), ref.view(np.uint32))
+        if full:
+            ok = ok and np.array_equal(med[b] if batch > 1 else med, rmed)
     done += 1
     if not ok:
-        bad.append({"n": n, "A": A, "kind": kind, "sampler": sampler, "full": full})
+        bad.append({"n": n, "A": A, "a0": a0, "a_count": a_count, "batch": batch, "kind": kind,
+                    "sampler": sampler, "full": full})
 ctx.destroy()
 print(json.dumps({"configs": done, "mismatches": len(bad), "first_bad": bad[:5]}))
 sys.exit(1 if bad else 0)
