@@ -43,7 +43,7 @@ def test_pfft_of_trace_sinograms_within_rtol_of_f64_fft(ctx, n, A, kind):
     assert np.all(np.abs(got - ref) <= RTOL * np.abs(ref) + 1e-30), np.max(np.abs(got - ref) / (ref + 1e-30))
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 16, 8192, 16384])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 16, 1000, 4095, 4097, 8192, 16384])
 def test_pfft_edge_lengths(ctx, n):
     rng = np.random.default_rng(n)
     rows = rng.random((3, n)).astype(np.float32)
