@@ -240,8 +240,12 @@ tt_status tt_tld4_probe(unsigned* d_out, int blocks, int iters, void* stream);
 /* Raw device-pointer entry (multi-GPU driver, benchmarks): enqueue the fused
  * kernel for a_count angles on `stream` (cudaStream_t; NULL = legacy
  * default).  out: full ? [a_count][6][n] : [a_count][n]; med may be NULL.
- * sampler: 0 = global/L1 loads, 1 = texture gather (a cudaArray copy of img
- * is made and released by this call).
+ * sampler: 0 = global/L1 loads (asynchronous: the call only enqueues), 1 =
+ * texture gather through a cudaArray copy of img that this call makes and
+ * releases -- which makes sampler 1 SYNCHRONOUS (the call waits for the
+ * launch before freeing the copy).  Asynchronous texture launches go through
+ * tt_image_tex_create + tt_trace_device_tex (the copy outlives the call);
+ * that is what the plans and the multi-GPU driver use.
  * pair_stride: 0 = the drop-in rule (angles [a0, a0+a_count); pairs
  * (a0+i, a0+i+a_count/2) when a_count is even); -1 = no pairing; > 0 = the
  * angles are a0+i and a0+i+pair_stride for i < a_count/2 (rows i and
@@ -326,6 +330,12 @@ tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, voi
  * VPTX bodies at tt_get_function: VPTX -> CUDA C++ -> NVRTC -> sm_100a).  This
  * returns the generated CUDA C++ for `kernel` without compiling (diagnostics). */
 tt_status tt_jit_source(const char* vptx, size_t len, const char* kernel, char* buf, size_t cap, size_t* needed);
+/* Fingerprint of a kernel body (FNV-1a over its token stream).  A module whose
+ * kernel has a body binds to a native kernel of the same signature only when
+ * this fingerprint is one the native kernel is registered for (trace_t05: the
+ * reference front end's compilation of the documented DSL trace kernel);
+ * any other body is compiled and run as written. */
+tt_status tt_vptx_body_fingerprint(const char* vptx, size_t len, const char* kernel, uint64_t* out);
 
 /* ---- plans: the host-to-host form of the path -------------------------------
  * One plan = one (n, angles, functionals, batch) configuration with its device

@@ -62,6 +62,11 @@ def lib():
         L.tto_check.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp,
                                 ctypes.c_int, fp, ip, ctypes.c_double, ctypes.c_int, ctypes.c_double, dp, ctypes.c_int]
         L.tto_check.restype = ctypes.c_long
+        L.tto_replay_units.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp, fp, fp, ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_int, ip, ip, fp, ip, ctypes.c_int]
+        L.tto_check_lines.argtypes = [fp, ctypes.c_int, fp, fp, fp, ctypes.c_int, ctypes.c_int, ip, ip, fp, ip,
+                                      ctypes.c_double, ctypes.c_int, ctypes.c_double, dp, ctypes.c_int]
+        L.tto_check_lines.restype = ctypes.c_long
         _lib = L
     return _lib
 
@@ -125,6 +130,42 @@ def replay_launch(img, n, ctab, stab, wtab, *, a0, units, pair_stride, full=True
     lib().tto_replay_launch(_f(np.ascontiguousarray(img, np.float32)), n, a0, units, pair_stride, _f(ctab),
                             _f(stab), _f(wtab), int(full), W, _f(out), _p(med, ctypes.c_int32), nthreads)
     return out, (med if full else None)
+
+
+def replay_units(img, n, ctab, stab, wtab, *, a0, pair_stride, units_idx, lines, full=True, W=0, nthreads=0):
+    """Replay of selected units (a0 + units_idx[k], lines[k]) of one launch.  Returns
+    (out f32 [k][2][F], med i32 [k][2][2], partner_col [k]): the unit's line and its partner
+    line (a0+ui+pair_stride, partner_col) -- n-1-p when the tables are exactly mirrored, else p;
+    bit-identical to tto_replay_launch's rows."""
+    ui = np.ascontiguousarray(units_idx, np.int32)
+    pl = np.ascontiguousarray(lines, np.int32)
+    F = NF if full else 1
+    out = np.zeros((len(ui), 2, F), np.float32)
+    med = np.zeros((len(ui), 2, 2), np.int32)
+    lib().tto_replay_units(_f(np.ascontiguousarray(img, np.float32)), n, a0, pair_stride, _f(ctab), _f(stab),
+                           _f(wtab), int(full), W, len(ui), _p(ui, ctypes.c_int32), _p(pl, ctypes.c_int32),
+                           _f(out), _p(med, ctypes.c_int32), nthreads)
+    pcol = pl.copy()
+    if pair_stride > 0:
+        a = a0 + ui
+        cb, sb = np.asarray(ctab, np.float32).view(np.uint32), np.asarray(stab, np.float32).view(np.uint32)
+        mir = (cb[a + pair_stride] == (cb[a] ^ 0x80000000)) & (sb[a + pair_stride] == (sb[a] ^ 0x80000000))
+        pcol = np.where(mir, n - 1 - pl, pl).astype(np.int32)
+    return out, (med if full else None), pcol
+
+
+def check_lines(img, n, ctab, stab, wtab, a_list, p_list, gpu_out, gpu_med=None, *, full=True, rtol=1e-4, W=0,
+                chain=0.0, nthreads=0):
+    """Spec §2.5 checker on an explicit list of lines: gpu_out [k][F], gpu_med [k][2]."""
+    a = np.ascontiguousarray(a_list, np.int32)
+    p = np.ascontiguousarray(p_list, np.int32)
+    st = np.zeros(4, np.float64)
+    gm = None if gpu_med is None else np.ascontiguousarray(gpu_med, np.int32)
+    fails = lib().tto_check_lines(_f(np.ascontiguousarray(img, np.float32)), n, _f(ctab), _f(stab), _f(wtab),
+                                  int(full), len(a), _p(a, ctypes.c_int32), _p(p, ctypes.c_int32),
+                                  _f(np.ascontiguousarray(gpu_out, np.float32)), _p(gm, ctypes.c_int32), rtol, W,
+                                  chain, _p(st, ctypes.c_double), nthreads)
+    return int(fails), {"worst": float(st[0]), "ties": int(st[1]), "median_bad": int(st[2]), "lines": int(st[3])}
 
 
 def circus(sino, nthreads=0):

@@ -506,6 +506,48 @@ void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stri
     }
 }
 
+/* Replay of selected units of one launch (large configurations whose full
+ * replay is too slow on the host): unit (a0 + ui[k], p[k]) with the launch's
+ * pairing, outputs out[k][2][F] (line (a0+ui, p), then its partner line:
+ * (a0+ui+pair_stride, n-1-p) when mirrored, (a0+ui+pair_stride, p) otherwise)
+ * and med[k][2][2].  Same arithmetic as tto_replay_launch. */
+void tto_replay_units(const float* img, int n, int a0, int pair_stride, const float* ctab, const float* stab,
+                      const float* wtab, int full, int NS, int count, const int32_t* ui, const int32_t* pl,
+                      float* out, int32_t* med, int nthreads) {
+    if (NS <= 0) NS = tto_schedule_slots(n, full);
+    const int F = full ? TTO_NF : 1;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel
+    {
+        float* buf = (float*)malloc(sizeof(float) * 4 * (size_t)(n > 0 ? n : 1));
+        float* o = (float*)calloc((size_t)2 * F * (n > 0 ? n : 1), sizeof(float));
+        int32_t* m = (int32_t*)calloc((size_t)2 * 2 * (n > 0 ? n : 1), sizeof(int32_t));
+#pragma omp for schedule(dynamic, 4)
+        for (int k = 0; k < count; ++k) {
+            const int a = a0 + ui[k], p = pl[k];
+            replay_unit(img, n, a, 1, pair_stride, ctab, stab, wtab, full, NS, 0, p, buf, buf + n,
+                        buf + 2 * (size_t)n, buf + 3 * (size_t)n, o, full ? m : NULL);
+            const int mir = pair_stride > 0 && mirrored(ctab, stab, a, a + pair_stride);
+            const int cols[2] = {p, mir ? n - 1 - p : p};
+            for (int li = 0; li < 2; ++li)
+                for (int f = 0; f < F; ++f) {
+                    out[((size_t)k * 2 + li) * F + f] = (li == 1 && pair_stride <= 0) ? 0.0f
+                                                        : o[((size_t)li * F + f) * n + cols[li]];
+                    if (med && full && f < 2)
+                        med[((size_t)k * 2 + li) * 2 + f] = (li == 1 && pair_stride <= 0) ? 0
+                                                            : m[((size_t)li * 2 + f) * n + cols[li]];
+                }
+        }
+        free(buf);
+        free(o);
+        free(m);
+    }
+}
+
 /* The structure the native trace_t05 / radon launcher uses for a launch of
  * a_count angles from a0: pairs (a0+i, a0+i+a_count/2) when a_count is even. */
 void tto_launch_structure(int a_count, int* units, int* pair_stride) {
@@ -651,16 +693,65 @@ static int is_eps_median(const float* v, int n, int m, double eps) {
     return reaches && not_before;
 }
 
+/* One line (a, p) against the f64 truth: gpu values g[f] (F of them), medians gm[2]
+ * (NULL: not checked).  Adds to the counters; returns the worst error ratio. */
+static double check_line(const float* img, int n, float c, float s_, int p, const float* wtab, int full,
+                         const float* g, int gstride, const int32_t* gm, int mstride, double rtol, double atol_c,
+                         double eps, float* v, float* sv, long* fails, long* ties, long* medbad) {
+    const int F = full ? TTO_NF : 1;
+    tto_line_samples(img, n, c, s_, p, v);
+    double o64[6], am[6];
+    int32_t md[2] = {0, 0};
+    if (full) {
+        tto_line_f64(v, n, wtab, -1, -1, o64, am, md);
+        if (gm) {
+            const int m0 = gm[0], m1 = gm[mstride];
+            int ok_m = (m0 == md[0]), ok_mp = (m1 == md[1]);
+            if (!ok_m || !ok_mp) {
+                for (int t = 0; t < n; ++t) sv[t] = sqrtf(v[t]);
+                if (!ok_m) ok_m = is_eps_median(v, n, m0, eps);
+                if (!ok_mp) ok_mp = is_eps_median(sv, n, m1, eps);
+                if (ok_m && ok_mp) {
+                    ++*ties;
+                    tto_line_f64(v, n, wtab, m0, m1, o64, am, md);
+                } else {
+                    ++*medbad;
+                    ++*fails;
+                    return 1e300;
+                }
+            }
+        }
+    } else {
+        double S = 0.0;
+        for (int t = 0; t < n; ++t) S += (double)v[t];
+        o64[0] = S;
+        am[0] = S;
+    }
+    double worst = 0.0;
+    for (int f = 0; f < F; ++f) {
+        const double gv = (double)g[(size_t)f * gstride];
+        const double tol = rtol * fabs(o64[f]) + atol_c * am[f] + 1e-30;
+        const double e = fabs(gv - o64[f]) / tol;
+        if (!(e <= 1.0)) ++*fails; /* NaN fails too */
+        if (e > worst || e != e) worst = (e != e) ? 1e300 : e;
+    }
+    return worst;
+}
+
+static double chain_of(int n, int W, double chain) {
+    const int NS = W > 0 ? W : tto_schedule_slots(n, 1);
+    const int K = (n + NS - 1) / NS;
+    /* fp32 chain length of the GPU schedule: slot partial + butterfly + groups
+     * (callers checking a sequential fp32 result pass chain = n) */
+    return chain > 0.0 ? chain : (double)K + 5.0 + (double)(NS / 32 + 1) + 4.0;
+}
+
 long tto_check(const float* img, int n, int a0, int a_count, int a_total, const float* ctab, const float* stab,
                const float* wtab, int full, const float* gpu_out, const int32_t* gpu_med, double rtol, int W,
                double chain, double* stats, int nthreads) {
     (void)a_total;
     const int F = full ? TTO_NF : 1;
-    const int NS = W > 0 ? W : tto_schedule_slots(n, 1);
-    const int K = (n + NS - 1) / NS;
-    /* fp32 chain length of the GPU schedule: slot partial + butterfly + groups
-     * (callers checking a sequential fp32 result pass chain = n) */
-    if (chain <= 0.0) chain = (double)K + 5.0 + (double)(NS / 32 + 1) + 4.0;
+    chain = chain_of(n, W, chain);
     const double u = 1.0 / 16777216.0;
     const double atol_c = 2.0 * chain * u;
     const double eps = 2.0 * chain * u; /* median tie window */
@@ -679,42 +770,10 @@ long tto_check(const float* img, int n, int a0, int a_count, int a_total, const 
 #pragma omp for schedule(dynamic, 64)
         for (long L = 0; L < lines; ++L) {
             const int ai = (int)(L / n), p = (int)(L % n), a = a0 + ai;
-            tto_line_samples(img, n, ctab[a], stab[a], p, v);
-            double o64[6], am[6];
-            int32_t md[2] = {0, 0};
-            if (full) {
-                tto_line_f64(v, n, wtab, -1, -1, o64, am, md);
-                if (gpu_med) {
-                    int gm = gpu_med[((size_t)ai * 2 + 0) * n + p];
-                    int gmp = gpu_med[((size_t)ai * 2 + 1) * n + p];
-                    int ok_m = (gm == md[0]), ok_mp = (gmp == md[1]);
-                    if (!ok_m || !ok_mp) {
-                        for (int t = 0; t < n; ++t) sv[t] = sqrtf(v[t]);
-                        if (!ok_m) ok_m = is_eps_median(v, n, gm, eps);
-                        if (!ok_mp) ok_mp = is_eps_median(sv, n, gmp, eps);
-                        if (ok_m && ok_mp) {
-                            ++ties;
-                            tto_line_f64(v, n, wtab, gm, gmp, o64, am, md);
-                        } else {
-                            ++medbad;
-                            ++fails;
-                            continue;
-                        }
-                    }
-                }
-            } else {
-                double S = 0.0;
-                for (int t = 0; t < n; ++t) S += (double)v[t];
-                o64[0] = S;
-                am[0] = S;
-            }
-            for (int f = 0; f < F; ++f) {
-                double g = (double)gpu_out[((size_t)ai * F + f) * n + p];
-                double tol = rtol * fabs(o64[f]) + atol_c * am[f] + 1e-30;
-                double e = fabs(g - o64[f]) / tol;
-                if (!(e <= 1.0)) ++fails; /* NaN fails too */
-                if (e > worst || e != e) worst = (e != e) ? 1e300 : e;
-            }
+            const double e = check_line(img, n, ctab[a], stab[a], p, wtab, full, gpu_out + (size_t)ai * F * n + p, n,
+                                        gpu_med ? gpu_med + (size_t)ai * 2 * n + p : NULL, n, rtol, atol_c, eps, v, sv,
+                                        &fails, &ties, &medbad);
+            if (e > worst) worst = e;
         }
         free(v);
         free(sv);
@@ -724,6 +783,44 @@ long tto_check(const float* img, int n, int a0, int a_count, int a_total, const 
         stats[1] = (double)ties;
         stats[2] = (double)medbad;
         stats[3] = (double)lines;
+    }
+    return fails;
+}
+
+long tto_check_lines(const float* img, int n, const float* ctab, const float* stab, const float* wtab, int full,
+                     int count, const int32_t* a_list, const int32_t* p_list, const float* gpu_out,
+                     const int32_t* gpu_med, double rtol, int W, double chain, double* stats, int nthreads) {
+    const int F = full ? TTO_NF : 1;
+    chain = chain_of(n, W, chain);
+    const double u = 1.0 / 16777216.0;
+    const double atol_c = 2.0 * chain * u, eps = 2.0 * chain * u;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    long fails = 0, ties = 0, medbad = 0;
+    double worst = 0.0;
+#pragma omp parallel reduction(+ : fails, ties, medbad) reduction(max : worst)
+    {
+        float* v = (float*)malloc(sizeof(float) * (size_t)n);
+        float* sv = (float*)malloc(sizeof(float) * (size_t)n);
+#pragma omp for schedule(dynamic, 16)
+        for (int k = 0; k < count; ++k) {
+            const int a = a_list[k];
+            const double e = check_line(img, n, ctab[a], stab[a], p_list[k], wtab, full, gpu_out + (size_t)k * F, 1,
+                                        gpu_med ? gpu_med + (size_t)k * 2 : NULL, 1, rtol, atol_c, eps, v, sv, &fails,
+                                        &ties, &medbad);
+            if (e > worst) worst = e;
+        }
+        free(v);
+        free(sv);
+    }
+    if (stats) {
+        stats[0] = worst;
+        stats[1] = (double)ties;
+        stats[2] = (double)medbad;
+        stats[3] = (double)count;
     }
     return fails;
 }

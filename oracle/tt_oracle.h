@@ -82,6 +82,13 @@ void tto_replay_launch(const float* img, int n, int a0, int units, int pair_stri
                        const float* stab, const float* wtab, int full, int NS, float* out, int32_t* med,
                        int nthreads);
 
+/* Replay of selected units (a0+ui[k], p[k]) of a launch with the given pairing:
+ * out[k][2][F] = the unit's line and its partner line (zeros when unpaired),
+ * med[k][2][2]; bit-identical to the same rows of tto_replay_launch. */
+void tto_replay_units(const float* img, int n, int a0, int pair_stride, const float* ctab, const float* stab,
+                      const float* wtab, int full, int NS, int count, const int32_t* ui, const int32_t* p,
+                      float* out, int32_t* med, int nthreads);
+
 /* Launch structure the native trace_t05/radon launcher uses for a_count
  * angles: pairs (i, i + a_count/2) when a_count is even. */
 void tto_launch_structure(int a_count, int* units, int* pair_stride);
@@ -115,6 +122,12 @@ long tto_check(const float* img, int n, int a0, int a_count, int a_total,
                const float* ctab, const float* stab, const float* wtab, int full,
                const float* gpu_out, const int32_t* gpu_med, double rtol, int W, double chain,
                double* stats, int nthreads);
+
+/* tto_check for an explicit list of lines (a_list[k], p_list[k]) with GPU values
+ * gpu_out[k][F] and medians gpu_med[k][2] (may be NULL). */
+long tto_check_lines(const float* img, int n, const float* ctab, const float* stab, const float* wtab, int full,
+                     int count, const int32_t* a_list, const int32_t* p_list, const float* gpu_out,
+                     const int32_t* gpu_med, double rtol, int W, double chain, double* stats, int nthreads);
 
 #ifdef __cplusplus
 }

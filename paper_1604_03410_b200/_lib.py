@@ -122,6 +122,7 @@ _sigs = {
     "tt_image_tex_destroy": (_S, [C.c_void_p]),
     "tt_trace_device_tex": (_S, [C.POINTER(TraceDesc), C.c_void_p, C.c_void_p]),
     "tt_jit_source": (_S, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "tt_vptx_body_fingerprint": (_S, [C.c_char_p, C.c_size_t, C.c_char_p, C.POINTER(C.c_uint64)]),
     "tt_plan_create": (_S, [C.c_void_p, C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]),
     "tt_plan_run": (_S, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tt_plan_submit": (_S, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

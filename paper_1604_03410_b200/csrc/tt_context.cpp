@@ -409,7 +409,7 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
             te.n = n;
             te.batch = batch;
             te.gen = img.gen;
-        } else if (te.gen != img.gen) {  // image rewritten since the copy: refresh (stream-ordered)
+        } else if (te.gen != img.gen || img.exported) {  // image (maybe) rewritten since the copy: refresh
             cudaError_t e = batch > 1 ? tt::fill_image_atlas(te.arr, ta.img, n, batch, (long long)N * N, te.cols,
                                                               ctx.stream)
                                       : cudaMemcpy2DToArrayAsync(te.arr, 0, 0, ta.img, std::size_t(n) * 4,
@@ -424,7 +424,7 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     int extra_launches = 0;
     if (full) {
         WeightEntry& we = ctx.w_cache[wt->base];
-        if (we.d == nullptr || we.n != n || we.gen != wt->gen) {
+        if (we.d == nullptr || we.n != n || we.gen != wt->gen || wt->exported) {
             if (we.d == nullptr || we.n != n) {
                 if (we.d) cudaFreeAsync(we.d, ctx.stream);
                 we = WeightEntry{};
@@ -512,6 +512,10 @@ Param P(bool ptr, Scalar t, const char* name, bool written = false) {
     return p;
 }
 
+// body_fingerprint() of tests/golden/trace_t05.vptx, the reference front end's compilation of
+// oracle/trace_t05.krn (checked by tests/test_jit_cpu.py).
+constexpr std::uint64_t kTraceT05BodyFingerprint = 0x64a3da5074adf4b3ull;
+
 const std::vector<NativeKernel>& registry() {
     static const std::vector<NativeKernel> reg = [] {
         std::vector<NativeKernel> r;
@@ -520,9 +524,7 @@ const std::vector<NativeKernel>& registry() {
             nk.decl.name = name;
             nk.decl.params = std::move(ps);
             nk.fn = fn;
-            const std::string nm = name;
-            nk.replaces_body = nm == "trace_t05" || nm == "trace_t05_batch" || nm == "radon" || nm == "circus" ||
-                               nm == "circus_fft";
+            if (std::string(name) == "trace_t05") nk.body_fingerprints = {kTraceT05BodyFingerprint};
             r.push_back(std::move(nk));
         };
         const Scalar f = Scalar::F32, d = Scalar::F64, i = Scalar::I32, l = Scalar::I64;
@@ -731,7 +733,11 @@ tt_status tt_get_function(tt_ctx* ctx, tt_module m, const char* name, tt_functio
     const bool header_only =
         decl->body.empty() || (decl->body.size() == 1 && decl->body[0].toks.size() == 1 && decl->body[0].toks[0] == "ret");
     const NativeKernel* nk = find_native(*decl);
-    if (nk && !header_only && !nk->replaces_body) nk = nullptr;  // run the module's own body
+    if (nk && !header_only) {  // a real body binds natively only if it is the documented DSL body
+        const std::uint64_t fp = body_fingerprint(decl->body);
+        if (std::find(nk->body_fingerprints.begin(), nk->body_fingerprints.end(), fp) == nk->body_fingerprints.end())
+            nk = nullptr;  // run the module's own body
+    }
     std::shared_ptr<JitFunction> jf;
     if (!nk) {
         if (header_only)
@@ -844,7 +850,8 @@ tt_status tt_mem_device_pointer(tt_ctx* ctx, tt_devptr p, void** out) {
     Alloc* a = nullptr;
     tt_status st = lookup(ctx, p, &a);
     if (st != TT_OK) return st;
-    ++a->gen;  // the caller may write through the raw pointer: cached copies are stale
+    ++a->gen;  // the caller may write through the raw pointer, now or later: cached copies are stale,
+    a->exported = true;  // and stay suspect for the allocation's lifetime (refreshed per launch)
     *out = a->dptr;
     return TT_OK;
 }
@@ -987,6 +994,7 @@ tt_status tt_launch(tt_ctx* ctx, tt_function fn, const tt_grid* cfg, const tt_ar
             ra[i].bytes = a->bytes;
             ra[i].base = args[i].v.ptr.base;
             ra[i].gen = a->gen;
+            ra[i].exported = a->exported;
         } else if (args[i].kind < TT_ARG_I32 || args[i].kind > TT_ARG_PTR) {
             return fail(ctx, TT_ERR_INVALID, "bad tt_arg kind");
         }
@@ -1100,6 +1108,36 @@ tt_status tt_events(tt_ctx* ctx, std::uint8_t* buf, std::size_t cap, std::size_t
 }
 
 }  // extern "C"
+
+std::uint64_t ttc::body_fingerprint(const std::vector<tt::jit::Line>& body) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&](unsigned char c) {
+        h ^= c;
+        h *= 1099511628211ull;
+    };
+    for (const auto& l : body) {
+        for (const auto& t : l.toks) {
+            for (unsigned char c : t) mix(c);
+            mix(0x1f);
+        }
+        mix('\n');
+    }
+    return h;
+}
+
+extern "C" tt_status tt_vptx_body_fingerprint(const char* vptx, std::size_t len, const char* kernel,
+                                              std::uint64_t* out) {
+    if (!vptx || !kernel || !out) return fail(nullptr, TT_ERR_INVALID, "null argument");
+    Module m;
+    tt_status st = parse_module(nullptr, vptx, len, m);
+    if (st != TT_OK) return st;
+    for (const auto& k : m.kernels)
+        if (k.name == kernel) {
+            *out = body_fingerprint(k.body);
+            return TT_OK;
+        }
+    return fail(nullptr, TT_ERR_FUNCTION_NOT_FOUND, std::string("FunctionNotFound: '") + kernel + "'");
+}
 
 extern "C" tt_status tt_jit_source(const char* vptx, std::size_t len, const char* kernel, char* buf, std::size_t cap,
                                    std::size_t* needed) {

@@ -66,6 +66,7 @@ struct ResolvedArg {
     std::uint64_t bytes = 0;
     std::uint64_t base = 0;  // synthetic address (allocation key)
     std::uint64_t gen = 0;   // write generation of the allocation
+    bool exported = false;   // its raw pointer was handed out (Alloc::exported)
 };
 
 struct LaunchOutcome {
@@ -79,11 +80,17 @@ using LaunchFn = LaunchOutcome (*)(tt_ctx&, const tt_grid&, const std::vector<Re
 struct NativeKernel {
     KernelDecl decl;
     LaunchFn fn;
-    // The fused trace kernels stand in for their documented DSL bodies (oracle/trace_t05.krn,
-    // bit-exact vs the reference engine) whatever body a module carries; the sample kernels only
-    // bind to header-only modules -- a module with a real VPTX body runs that body (JIT).
-    bool replaces_body = false;
+    // A module binds to the native kernel when its kernel is header-only, or when its VPTX body
+    // is one of the documented DSL bodies the native kernel stands in for, identified by
+    // body_fingerprint() (trace_t05: oracle/trace_t05.krn as the reference front end compiles
+    // it, tests/golden/trace_t05.vptx).  Any other body runs as written (JIT): a user kernel that
+    // merely shares a name and signature is never replaced.
+    std::vector<std::uint64_t> body_fingerprints;
 };
+
+// FNV-1a 64 over a kernel body's token stream (tokens separated by 0x1f, lines by '\n'):
+// invariant under whitespace and comments, sensitive to every instruction and operand.
+std::uint64_t body_fingerprint(const std::vector<tt::jit::Line>& body);
 
 
 // ---------------------------------------------------------------- context
@@ -93,6 +100,9 @@ struct Alloc {
     std::uint64_t bytes = 0;
     bool live = true;
     std::uint64_t gen = 0;  // bumped by every write (H2D copy, written launch argument)
+    bool exported = false;  // raw pointer handed out (tt_mem_device_pointer): writes are invisible to
+                            // the context, so cached derived copies (texture, weight layout) are
+                            // refreshed at every launch that reads this allocation
 };
 
 // Texture-gather sampler state cached per image allocation: the block-linear

@@ -139,3 +139,23 @@ def test_jit_of_the_reference_dsl_trace_kernel_equals_seq32_oracle(ctx, n, A, ki
     rout, rmed, _, _ = O.transform(img, n, c, s, w, mode=O.SEQ32)
     assert np.array_equal(out.view(np.uint32), rout.view(np.uint32))
     assert np.array_equal(med, rmed)
+
+
+def test_foreign_body_with_a_native_name_runs_as_written(ctx):
+    """A user kernel that only shares the name and signature of a native kernel is compiled from
+    its own body (no silent substitution): here a `trace_t05` whose body writes 7.0 to out[0]."""
+    header = TRACE_VPTX.split("{", 1)[0]  # .module + .kernel with the native signature
+    vptx = (header + "{\n  .reg f32 %v\n  .reg i64 %a\n  mov.f32 %v, 0f40E00000\n  mov.i64 %a, out\n"
+            "  st.global.f32 [%a], %v\n  ret\n}\n")
+    mh = ctx.module_load(vptx)
+    fn = ctx.get_function(mh, "trace_t05")
+    n = 8
+    bufs = [ctx.mem_alloc(64 * 4) for _ in range(6)]
+    res = ctx.launch(fn, tt.GridConfig((1, 1, 1), (1, 1, 1)),
+                     [bufs[0], np.int32(n), bufs[1], bufs[2], bufs[3], bufs[4], bufs[5], np.int32(0)])
+    assert res.ok(), res.trap
+    out = np.empty(64, np.float32)
+    ctx.memcpy_dtoh(out, bufs[4])
+    assert out[0] == 7.0 and not out[1:].any()
+    for b in bufs:
+        ctx.mem_free(b)
