@@ -1,18 +1,22 @@
 #!/usr/bin/env python
 """Trace-transform benchmark (contract: one JSON line from rank 0).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c2|c1|c4]
                   [--impl ours|reference] [--sampler 0|1]
 
 Metric: sinogram samples/s = F*A*n per image per second (F = 6 for T0..T5),
 whole job over all ranks.  A "step" is one pass of the hot path over one
 image of the workload:
-  c2 (default, BASELINE.json configs[1]): 1024^2 image, 720 angles, T0..T5;
-     N>1: one image per rank ("image batches sharded", weak scaling), the
-     per-rank feature summaries gathered to rank 0 over NCCL.
-  c3: 4096^2 image, 1440 angles, T0..T5; N>1: orientations sharded across
-     ranks (strong scaling), sinogram slices all-gathered over NCCL.
+  c3 (default; BASELINE.json configs[2], the north_star's target workload):
+     4096^2 image, 1440 angles, T0..T5; N>1: orientations sharded across ranks
+     (strong scaling; paper_1604_03410_b200.sharded.ShardedTrace: the shard
+     kernels write into rank 0's sinogram over NVLink P2P).
+  c2 (configs[1]): 1024^2 image, 720 angles, T0..T5 + P-functionals (circus);
+     N>1: one image per rank (weak scaling), features gathered over NCCL.
   c1: 256^2, 360 angles (the reference's CPU-runnable case).
+  c4: 4096 x 256^2 images, 360 angles, T0..T5 + circus, images sharded.
+A plain `python bench.py --gpus N` (no WORLD_SIZE) spawns the N ranks itself
+through torch.distributed.run.
 `value` times the fused kernel on device-resident inputs (CUDA events on the
 launching stream, L2 flushed between steps, max over ranks); `e2e` times the
 public API (tt.Plan.run / tt_plan_run: pinned H2D of the image, the chunked launches,
@@ -37,11 +41,13 @@ WORKLOADS = {
     "c1": dict(n=256, angles=360, full=True, features=False, desc="256^2 fp32, 360 angles x 256 lines, T0-T5"),
     "c2": dict(n=1024, angles=720, full=True, features=True,
                desc="1024^2 fp32, 720 angles x 1024 lines, T0-T5 + P-functionals (circus)"),
-    "c3": dict(n=4096, angles=1440, full=True, features=False, desc="4096^2 fp32, 1440 angles x 4096 lines, T0-T5"),
+    "c3": dict(n=4096, angles=1440, full=True, features=False, orient=True,
+               desc="4096^2 fp32, 1440 angles x 4096 lines, T0-T5"),
     "c4": dict(n=256, angles=360, full=True, features=True, batch=4096,
                desc="batched feature extraction: 4096 x 256^2 fp32, 360 angles, T0-T5 + circus"),
 }
 FLOPS_PER_TAP = {True: 34, False: 16}  # FMA = 2, in-bounds taps only
+FLOPS_PER_TAP_EXEC = {True: 26, False: 9}  # the same, the sampling flops counted once per mirrored pair
 METRIC = "trace-transform sinogram samples/s"
 UNIT = "samples/s"
 
@@ -160,27 +166,39 @@ def load_traffic(workload: str):
     return j.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT), pipes
 
 
+def cpu_model() -> str:
+    """The host CPU model (lscpu "Model name"), for the cpu_baseline / reference lines."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(wl, seconds_target=10.0):
     """The oracle port (TTO_SEQ32 sampler + functionals, and the circus stage
-    when the workload has it; OpenMP over lines on all host threads) on a
-    bounded sample of the same workload: whole images repeated (or a prefix of
-    the angles) until about `seconds_target` of CPU work."""
+    when the workload has it; OpenMP over lines) on a bounded sample of the
+    same workload: a prefix of the angles of one image, repeated until about
+    `seconds_target` of CPU work on all host threads, then the same sample on
+    one thread (the 1-core figure)."""
     import oracle as O
-    import paper_1604_03410_b200 as tt
     n, A = wl["n"], wl["angles"]
-    img = tt.synth_image(tt.DISK, n)
-    c, s, w = tt.make_tables(n, A)
+    img = O.synth(O.DISK, n)
+    c, s, w = O.tables(n, A)
     cores = os.cpu_count() or 1
 
-    def run(a_count):
-        out, _, _, _ = O.transform(img, n, c, s, w, a0=0, a_count=a_count, mode=O.SEQ32, nthreads=cores)
+    def run(a_count, threads):
+        out, _, _, _ = O.transform(img, n, c, s, w, a0=0, a_count=a_count, mode=O.SEQ32, nthreads=threads)
         if wl.get("features"):
-            O.circus(out, nthreads=cores)
+            O.circus(out, nthreads=threads)
 
     a_count, t = 1, 0.0
     while True:
         t0 = time.perf_counter()
-        run(a_count)
+        run(a_count, cores)
         t = time.perf_counter() - t0
         if t >= seconds_target / 4 or a_count >= A:
             break
@@ -188,13 +206,21 @@ def cpu_baseline(wl, seconds_target=10.0):
     reps = max(1, int(seconds_target / max(t, 1e-3)))
     t0 = time.perf_counter()
     for _ in range(reps):
-        run(a_count)
+        run(a_count, cores)
     t = time.perf_counter() - t0
     samples = 6 * a_count * n * reps
+    # 1 core: the smallest angle prefix that takes >= ~2 s, one pass
+    a1 = max(1, min(a_count, int(a_count * 2.0 / max(t / reps * cores, 1e-3)) + 1))
+    t1 = time.perf_counter()
+    run(a1, 1)
+    t1 = time.perf_counter() - t1
     return {"value": samples / t, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(), "nproc": cores,
+            "value_1core": 6 * a1 * n / t1,
             "sample": f"oracle TTO_SEQ32 (sequential fp32, pinned sampler){' + circus' if wl.get('features') else ''}"
                       f" on {a_count} of {A} angles x {n} lines of one {n}^2 image, repeated {reps}x "
-                      f"({t:.1f} s wall, OpenMP {cores} threads)",
+                      f"({t:.1f} s wall, OpenMP {cores} threads); 1-core figure: {a1} angles, one pass "
+                      f"({t1:.1f} s)",
             "seconds": t}
 
 
@@ -207,6 +233,7 @@ def run_ours(args, ws, rank, local):
     import paper_1604_03410_b200 as tt
     from paper_1604_03410_b200 import shard
     from paper_1604_03410_b200._lib import lib
+    from paper_1604_03410_b200.sharded import ShardedTrace
     from paper_1604_03410_b200.trace import image_atlas, image_texture, image_texture_destroy, image_texture_update
 
     if args.dev_one_gpu:
@@ -223,11 +250,10 @@ def run_ours(args, ws, rank, local):
     n, A, full, feats_on = wl["n"], wl["angles"], wl["full"], wl["features"]
     F = 6 if full else 1
     batch_total = wl.get("batch", 1)
-    orient = args.workload == "c3" and ws > 1        # orientation shards + sinogram gather (strong)
+    orient = wl.get("orient", False) and ws > 1      # orientation shards assembled on rank 0 (strong)
     images = batch_total > 1                         # image shards (strong over a fixed batch)
     h = A // 2
     if orient:
-        # rank r owns angles [a0, a0+cnt) and their mirrors [A/2+a0, ...) -> rows [cnt] + [cnt]
         a0, cnt, pair = shard.orientation_shard(A, ws, rank)
         a_cnt = 2 * cnt
     else:
@@ -237,67 +263,61 @@ def run_ours(args, ws, rank, local):
     else:
         b0, B = rank, 1  # c1/c2 under torchrun: one image per rank (weak scaling)
 
-    stream = torch.cuda.Stream()
-    sptr = stream.cuda_stream
     ctab_h, stab_h, wtab_h = tt.make_tables(n, A)
     seed0 = tt.SEEDS[tt.DISK]
     img_h = np.stack([tt.synth_image(tt.DISK, n, seed0 + (0 if orient else b0 + b)) for b in range(B)])
-    with torch.cuda.stream(stream):
-        img = torch.from_numpy(img_h).cuda()
-        ctab, stab, wtab = (torch.from_numpy(x).cuda() for x in (ctab_h, stab_h, wtab_h))
-        out = torch.empty((B, a_cnt, F, n), device="cuda")
-        med = torch.empty((B, a_cnt, 2, n), dtype=torch.int32, device="cuda")
-        circ = torch.empty((B, a_cnt, F, 3), device="cuda")
-        flush = torch.empty(int(256 << 20) // 4, device="cuda")  # > 126 MB L2
-        wsoa = torch.empty(6 * n, device="cuda") if full else None  # pass-2 weight layout (constant of n)
-        # orientation shards: rank 0 holds the assembled sinogram (+ medians); every rank's fused
-        # kernel writes its rows straight into it over NVLink P2P (CUDA IPC mapping)
-        gathered = torch.empty((A, F, n), device="cuda") if orient and rank == 0 else None
-        gmed = torch.empty((A, 2, n), dtype=torch.int32, device="cuda") if orient and rank == 0 else None
-        signal = torch.zeros(1, device="cuda") if orient else None
-        feats = torch.empty((ws * B, a_cnt, F, 3), device="cuda") if (ws > 1 and not orient) else None
+    flush = torch.empty(int(256 << 20) // 4, device="cuda")  # > 126 MB L2
     tex = None
-    if args.sampler == 1:  # texture layout of this step's image(s); refreshed inside every timed step
-        tex = image_atlas(img.data_ptr(), n, B, 0, sptr) if B > 1 else image_texture(img.data_ptr(), n, sptr)
-    if full:
-        tt.weights_soa(wtab.data_ptr(), n, wsoa.data_ptr(), sptr)
-    launches_per_step = 1 + (1 if feats_on else 0) + (1 if tex is not None and B > 1 else 0)
-
-    close_peer = None
+    st = None
     if orient:
-        peer, close_peer = shard.share_device_buffers(
-            [gathered.data_ptr(), gmed.data_ptr()] if rank == 0 else [], dist, local)
-        _, _, _, row0, prow = shard.direct_shard_rows(A, ws, rank, F, n)
-        out_ptr, med_ptr = peer[0] + row0 * F * n * 4, peer[1] + row0 * 2 * n * 4
+        # the multi-GPU public call: shard kernels write rows into rank 0's sinogram over NVLink P2P,
+        # per-chunk completion signals; the device leg starts with the image already on every GPU
+        st = ShardedTrace(n, A, dist, local, full=full, chunks=args.chunks or 4, sampler=args.sampler)
+        st.img[0].copy_(torch.from_numpy(img_h[0]))
+        torch.cuda.synchronize()
+        stream = st.stream
+        launches_per_step = st.chunks + (1 if args.sampler == 1 else 0)
+
+        def step():
+            st.run_device()
+
+        def features():
+            pass
     else:
-        out_ptr, med_ptr, prow = out.data_ptr(), med.data_ptr(), 0
-
-    def step():
-        if tex is not None:
-            image_texture_update(tex, img.data_ptr(), 0, sptr)
-        tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
-                        out_ptr, med_ptr, full=full, sampler=args.sampler, stream=sptr, tex=tex,
-                        pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0, partner_row=prow,
-                        peer_out=orient and rank != 0)
-
-    def features():
-        if feats_on:  # P-functional (circus) stage consuming the sinograms
-            tt.circus_device(out.data_ptr(), n, B * a_cnt * F, circ.data_ptr(), stream=sptr)
-
-    def exchange():
-        if not dist:
-            return
+        stream = torch.cuda.Stream()
+        sptr = stream.cuda_stream
         with torch.cuda.stream(stream):
-            if orient:  # rows already written into rank 0's sinogram by the kernels: 4-byte completion signal
-                dist.all_reduce(signal)
-            else:       # image sharding: gather the per-image circus features
-                dist.all_gather_into_tensor(feats, circ)
+            img = torch.from_numpy(img_h).cuda()
+            ctab, stab, wtab = (torch.from_numpy(x).cuda() for x in (ctab_h, stab_h, wtab_h))
+            out = torch.empty((B, a_cnt, F, n), device="cuda")
+            med = torch.empty((B, a_cnt, 2, n), dtype=torch.int32, device="cuda")
+            circ = torch.empty((B, a_cnt, F, 3), device="cuda")
+            wsoa = torch.empty(6 * n, device="cuda") if full else None  # pass-2 weight layout (constant of n)
+            feats = torch.empty((ws * B, a_cnt, F, 3), device="cuda") if ws > 1 else None
+        if args.sampler == 1:  # texture layout of this step's image(s); refreshed inside every timed step
+            tex = image_atlas(img.data_ptr(), n, B, 0, sptr) if B > 1 else image_texture(img.data_ptr(), n, sptr)
+        if full:
+            tt.weights_soa(wtab.data_ptr(), n, wsoa.data_ptr(), sptr)
+        launches_per_step = 1 + (1 if feats_on else 0) + (1 if tex is not None and B > 1 else 0)
+
+        def step():
+            if tex is not None:
+                image_texture_update(tex, img.data_ptr(), 0, sptr)
+            tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
+                            out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
+                            pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0)
+
+        def features():
+            if feats_on:  # P-functional (circus) stage consuming the sinograms
+                tt.circus_device(out.data_ptr(), n, B * a_cnt * F, circ.data_ptr(), stream=sptr)
+            if dist:      # image sharding: gather the per-image circus features
+                with torch.cuda.stream(stream):
+                    dist.all_gather_into_tensor(feats, circ)
 
     torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
         features()
-        exchange()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -317,7 +337,6 @@ def run_ours(args, ws, rank, local):
             step()
             ev[i][1].record(stream)
             features()
-            exchange()
             ev[i][2].record(stream)
         torch.cuda.synchronize()
         if dist:
@@ -339,86 +358,116 @@ def run_ours(args, ws, rank, local):
     value = samples_step / (ms_per_step / 1e3)
 
     # ---- e2e through the public API (host buffers, copies in the timed region) ----
-    ctx = tt.create_context(local)
-    ctx.set_sampler(args.sampler)
-    # public API on this rank's share (contiguous angle block under torchrun c3)
-    plan = tt.Plan(ctx, n, A, full=full, a0=rank * a_cnt if orient else 0, a_count=a_cnt, features=feats_on,
-                   batch=B)
-    nb_img, nb_out = B * n * n * 4, B * a_cnt * F * n * 4
-    nb_med, nb_circ = B * a_cnt * 2 * n * 4, B * a_cnt * F * 3 * 4
-    # feature extraction (c4) returns the features; the sinogram workloads return sinograms + medians
-    want_sino = not images
-    # pinned host buffers: one image, two output sets (consecutive submissions are in flight together)
-    nbs = (nb_img, nb_out if want_sino else 4, nb_med if want_sino else 4, nb_circ)
-    hp = [C.c_void_p() for _ in range(7)]
-    for hh, nb in zip(hp, nbs + nbs[1:]):
-        if lib.tt_host_alloc(nb, C.byref(hh)) != 0:
-            raise RuntimeError(f"tt_host_alloc({nb}) failed")
-    h_img = np.ctypeslib.as_array((C.c_float * (B * n * n)).from_address(hp[0].value)).reshape(img_h.shape)
-    h_img[:] = img_h
-    outs = []
-    for k in (1, 4):
-        outs.append((np.ctypeslib.as_array((C.c_float * (nb_out // 4)).from_address(hp[k].value)) if want_sino else None,
-                     np.ctypeslib.as_array((C.c_int32 * (nb_med // 4)).from_address(hp[k + 1].value))
-                     if want_sino and full else None,
-                     np.ctypeslib.as_array((C.c_float * (nb_circ // 4)).from_address(hp[k + 2].value))
-                     if feats_on else None))
-    img_arg = h_img if B > 1 else h_img[0]
-    for _ in range(max(2, min(args.warmup, 3) if images else args.warmup)):
-        plan.run(img_arg, *outs[0])
     e2e_steps = max(3, min(args.steps, 5 if images else 50))
-    if dist:
-        dist.barrier()
-    # every step: H2D of the image, the chunked launches, D2H of sinograms + medians (+ features);
-    # steps are submitted back to back (the next upload overlaps the current kernels) and drained
-    t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        plan.submit(img_arg, *outs[i % 2])
-    plan.wait()
-    e2e_pipelined_s = time.perf_counter() - t0
-    # and the latency of one synchronous call (tt_plan_run: submit + wait, nothing overlapped across calls)
     lat = []
-    for _ in range(min(10, e2e_steps)):
-        t1 = time.perf_counter()
-        plan.run(img_arg, *outs[0])
-        lat.append(time.perf_counter() - t1)
-    e2e_s = e2e_pipelined_s / e2e_steps  # pipelined throughput per step
+    if orient:
+        # ShardedTrace.submit: rank 0 uploads the pinned image, broadcasts it (NCCL), every shard's
+        # kernels write into rank 0's sinogram (P2P), rank 0 downloads the rows chunk by chunk
+        root = rank == 0
+        h_img = torch.from_numpy(img_h[0]).pin_memory() if root else None
+        h_out = torch.empty((A, F, n), pin_memory=True) if root else None
+        h_med = torch.empty((A, 2, n), dtype=torch.int32, pin_memory=True) if root else None
+        for _ in range(max(2, args.warmup)):
+            st.submit(h_img, h_out, h_med)
+        st.wait()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            st.submit(h_img, h_out, h_med)
+        st.wait()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        for _ in range(min(10, e2e_steps)):
+            dist.barrier()
+            t1 = time.perf_counter()
+            st.submit(h_img, h_out, h_med)
+            st.wait()
+            lat.append(time.perf_counter() - t1)
+        nb_img = n * n * 4 if root else 0
+        d2h = A * (F + (2 if full else 0)) * n * 4 if root else 0
+        chunks_note = f"{st.chunks} chunks per shard"
+        api = (f"ShardedTrace.submit/wait (per step: rank 0 pinned H2D of the image, NCCL broadcast, "
+               f"{chunks_note} of fused-kernel launches writing rows into rank 0's sinogram over NVLink P2P, "
+               f"a 4-byte completion all_reduce per chunk, rank 0 D2H of sinogram + medians overlapped "
+               f"chunk by chunk)")
+    else:
+        ctx = tt.create_context(local)
+        ctx.set_sampler(args.sampler)
+        plan = tt.Plan(ctx, n, A, full=full, a0=0, a_count=a_cnt, features=feats_on, batch=B)
+        nb_img, nb_out = B * n * n * 4, B * a_cnt * F * n * 4
+        nb_med, nb_circ = B * a_cnt * 2 * n * 4, B * a_cnt * F * 3 * 4
+        # feature extraction (c4) returns the features; the sinogram workloads return sinograms + medians
+        want_sino = not images
+        # pinned host buffers: one image, two output sets (consecutive submissions are in flight together)
+        nbs = (nb_img, nb_out if want_sino else 4, nb_med if want_sino else 4, nb_circ)
+        hp = [C.c_void_p() for _ in range(7)]
+        for hh, nb in zip(hp, nbs + nbs[1:]):
+            if lib.tt_host_alloc(nb, C.byref(hh)) != 0:
+                raise RuntimeError(f"tt_host_alloc({nb}) failed")
+        h_img = np.ctypeslib.as_array((C.c_float * (B * n * n)).from_address(hp[0].value)).reshape(img_h.shape)
+        h_img[:] = img_h
+        outs = []
+        for k in (1, 4):
+            outs.append((np.ctypeslib.as_array((C.c_float * (nb_out // 4)).from_address(hp[k].value))
+                         if want_sino else None,
+                         np.ctypeslib.as_array((C.c_int32 * (nb_med // 4)).from_address(hp[k + 1].value))
+                         if want_sino and full else None,
+                         np.ctypeslib.as_array((C.c_float * (nb_circ // 4)).from_address(hp[k + 2].value))
+                         if feats_on else None))
+        img_arg = h_img if B > 1 else h_img[0]
+        for _ in range(max(2, min(args.warmup, 3) if images else args.warmup)):
+            plan.run(img_arg, *outs[0])
+        if dist:
+            dist.barrier()
+        # every step: H2D of the image, the chunked launches, D2H of sinograms + medians (+ features);
+        # steps are submitted back to back (the next upload overlaps the current kernels) and drained
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            plan.submit(img_arg, *outs[i % 2])
+        plan.wait()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        # and the latency of one synchronous call (tt_plan_run: submit + wait, nothing overlapped across calls)
+        for _ in range(min(10, e2e_steps)):
+            t1 = time.perf_counter()
+            plan.run(img_arg, *outs[0])
+            lat.append(time.perf_counter() - t1)
+        d2h = (nb_out + (nb_med if full else 0) if want_sino else 0) + (nb_circ if feats_on else 0)
+        api = (f"tt.Plan.submit/wait -> tt_plan_submit x steps + tt_plan_wait (per step: pinned H2D, "
+               f"{plan.chunks} chunked fused-kernel launches with overlapped D2H of finished rows"
+               + (", circus" if feats_on else "") + "; two buffer slots, consecutive steps overlap)")
     if dist:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    d2h = (nb_out + (nb_med if full else 0) if want_sino else 0) + (nb_circ if feats_on else 0)
     e2e = {"value": samples_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nb_img, "d2h_bytes_per_step": d2h,
-           "ms_per_step": e2e_s * 1e3,
-           "sync_call_latency_ms": statistics.median(lat) * 1e3,
-           "api": f"tt.Plan.submit/wait -> tt_plan_submit x steps + tt_plan_wait (per step: pinned H2D, "
-                  f"{plan.chunks} chunked fused-kernel launches with overlapped D2H of finished rows"
-                  + (", circus" if feats_on else "") + "; two buffer slots, consecutive steps overlap)"}
-    # parity spot checks: the e2e output against the device-resident one; under orientation
-    # sharding, rank 0's P2P-assembled sinogram against one whole single-GPU launch
+           "ms_per_step": e2e_s * 1e3, "sync_call_latency_ms": statistics.median(lat) * 1e3, "api": api}
+
+    # ---- parity spot checks ----
     if orient:
         same = True
-        if rank == 0:
+        if rank == 0:  # the P2P-assembled sinogram (device and host copies) against one whole 1-GPU launch
             ref = torch.empty((A, F, n), device="cuda")
             rmed = torch.empty((A, 2, n), dtype=torch.int32, device="cuda")
-            tt.trace_device(img.data_ptr(), n, 0, A, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
-                            ref.data_ptr(), rmed.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
-                            wsoa_ptr=wsoa.data_ptr() if full else 0)
+            rimg = torch.from_numpy(img_h[0]).cuda()
+            tt.trace_device(rimg.data_ptr(), n, 0, A, st.ctab.data_ptr(), st.stab.data_ptr(), st.wtab.data_ptr(),
+                            ref.data_ptr(), rmed.data_ptr(), full=full, sampler=0,
+                            wsoa_ptr=st.wsoa.data_ptr() if full else 0)
             torch.cuda.synchronize()
-            same = bool(torch.equal(gathered.view(torch.int32), ref.view(torch.int32)) and torch.equal(gmed, rmed))
+            same = bool(torch.equal(st.out.view(torch.int32), ref.view(torch.int32)) and torch.equal(st.med, rmed)
+                        and torch.equal(h_out.view(torch.int32), ref.cpu().view(torch.int32))
+                        and torch.equal(h_med, rmed.cpu()))
             del ref, rmed
-        dist.barrier()
-        close_peer()
-    elif want_sino:
+        st.close()
+    elif not images:
         same = np.array_equal(outs[(e2e_steps - 1) % 2][0].reshape(out.shape), out.cpu().numpy())
     else:
         same = np.array_equal(outs[(e2e_steps - 1) % 2][2].reshape(circ.shape), circ.cpu().numpy())
-    plan.destroy()
-    ctx.destroy()
-    for hh in hp:
-        lib.tt_host_free(hh)
+    if not orient:
+        plan.destroy()
+        ctx.destroy()
+        for hh in hp:
+            lib.tt_host_free(hh)
 
-    # ---- roofline of the fused kernel (this rank's launch) ----
+    # ---- roofline of the fused kernel (this rank's launches) ----
     if orient:
         taps = lib.tt_count_inbounds_taps(n, a0, cnt, ctab_h.ctypes.data, stab_h.ctypes.data) + \
             lib.tt_count_inbounds_taps(n, a0 + h, cnt, ctab_h.ctypes.data, stab_h.ctypes.data)
@@ -426,27 +475,39 @@ def run_ours(args, ws, rank, local):
         taps = B * lib.tt_count_inbounds_taps(n, 0, A, ctab_h.ctypes.data, stab_h.ctypes.data)
     kern_s = statistics.mean(kern_ms) / 1e3
     peak = fp32_peak_tflops(torch, tt, stream)
-    achieved = FLOPS_PER_TAP[full] * taps / kern_s / 1e12
     traffic, traffic_src, pipes = load_traffic(args.workload)
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic,
-                "peak_source": "measured in this run: tt_ffma_probe (8 independent FFMA chains x 148*8 CTAs), "
-                               "FP32 is the bound (image L2-resident; no tensor-core work)",
-                "work": f"{FLOPS_PER_TAP[full]} flop per in-bounds tap x {taps} taps (SURVEY.md 8d)",
-                "kernel_ms": kern_s * 1e3, "taps_per_s": taps / kern_s,
-                "hbm_algorithmic_bytes": B * (n * n * 4 + a_cnt * (F + 2) * n * 4),
-                "traffic_source": traffic_src}
+    # executed-flop model (SURVEY.md 8d without double credit): the 16 sampling flops of a tap are
+    # executed once per mirrored PAIR of line taps -> 8 per line tap, + 18 per line tap for the
+    # prefix sums and the T1..T5 accumulations = 26 (T0 only: 16 / 2 + 1 = 9)
+    fpt = FLOPS_PER_TAP_EXEC[full]
+    fp32 = {"achieved": fpt * taps / kern_s / 1e12, "peak": peak, "unit": "TFLOP/s",
+            "frac": fpt * taps / kern_s / 1e12 / peak,
+            "work": f"{fpt} executed flop per in-bounds line tap x {taps} taps (mirrored pairs share the sampling)",
+            "peak_source": "measured in this run: tt_ffma_probe (8 independent FFMA chains x 148*8 CTAs)"}
+    # mirrored angle pairs share one sampling pass, so a launch issues B * (a_cnt / 2) * n^2 gathers
+    gpk = B * (a_cnt // 2) * n * n
+    if args.sampler == 1:
+        tpeak = tex_peak_gathers(torch, stream)
+        roofline = {"bound": "tex", "achieved": gpk / kern_s, "peak": tpeak, "unit": "gathers/s",
+                    "frac": gpk / kern_s / tpeak, "traffic": traffic,
+                    "work": f"{gpk} TLD4 gathers per launch: one per distinct sampled tap (mirrored angle pairs "
+                            f"share one sampling pass; in- and out-of-range taps)",
+                    "peak_source": "measured in this run: tt_tld4_probe (8 independent TLD4 per thread, "
+                                   "L1-resident texture, 148*8 CTAs)",
+                    "binding_unit_note": "ncu: SM issue slots and the L1/TEX data path (texture gathers + line-"
+                                         "buffer LDS/STS) are co-binding (see ncu_pipes); HBM is not (image "
+                                         "L2-resident / line-blocked order), so the sampling pipe is the roofline",
+                    "fp32_model": fp32}
+    else:
+        roofline = dict(bound="fp32", traffic=traffic, **fp32)
+    roofline.update({"kernel_ms": kern_s * 1e3, "taps_per_s": taps / kern_s,
+                     "hbm_algorithmic_bytes": B * (n * n * 4 + a_cnt * (F + 2) * n * 4),
+                     "traffic_source": traffic_src})
     if pipes:
         roofline["ncu_pipes"] = pipes
-    # the sampling stage's own roofline: one TLD4 lane-gather per sampled tap; mirrored angle pairs
-    # share one sampling pass, so a launch issues B * (a_cnt / 2) * n^2 gathers (in- and out-of-range)
-    if tex is not None:
-        gpk = B * (a_cnt // 2) * n * n
-        tpeak = tex_peak_gathers(torch, stream)
-        roofline["tex_gather"] = {"achieved": gpk / kern_s, "peak": tpeak, "unit": "gathers/s",
-                                  "frac": gpk / kern_s / tpeak, "gathers_per_launch": gpk,
-                                  "peak_source": "measured in this run: tt_tld4_probe (8 independent TLD4 per "
-                                                 "thread, L1-resident texture, 148*8 CTAs)"}
+    if orient:
+        roofline["kernel_ms_note"] = ("per-rank step time incl. the chunk signals (no separate kernel-only "
+                                      "event under orientation sharding)")
     scaling = "strong" if (orient or images) else "weak"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -457,15 +518,16 @@ def run_ours(args, ws, rank, local):
                        "functionals": ("T0-T5" if full else "T0") + (" + P1-P3 circus" if feats_on else ""),
                        "sampler": ["ldg", "tex"][args.sampler],
                        "parallelism": (f"orientations sharded x{ws}; fused kernels write sinogram rows into "
-                                       "rank 0 over NVLink P2P + 4-byte NCCL completion signal" if orient else
-                                       (f"images sharded x{ws} + NCCL feature gather" if ws > 1 else "1 GPU")),
+                                       "rank 0 over NVLink P2P + per-chunk 4-byte NCCL completion signal"
+                                       if orient else
+                                       (f"images sharded x{ws} + NCCL feature gather" if images and ws > 1 else
+                                        (f"one image per rank x{ws} + NCCL feature gather" if ws > 1 else
+                                         "1 GPU"))),
                        "l2": "flushed (256 MiB memset) between timed steps",
                        "ms_per_image": ms_per_step / (batch_total if images else 1)},
             "e2e": e2e, "roofline": roofline, "clocks": clocks.summary(),
             "gpu_launches": args.steps * launches_per_step,
-            "e2e_matches_device_result": None if orient else bool(same)}
-    if orient:
-        line["p2p_assembled_sinogram_matches_single_launch"] = bool(same)
+            "e2e_matches_device_result": bool(same)}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl)
     if tex is not None:
@@ -478,48 +540,88 @@ def run_ours(args, ws, rank, local):
 # ---------------------------------------------------------- reference arm
 
 def run_reference(args, ws, rank):
-    """The reference's own execution engine on a bounded sample (rank 0 only)."""
+    """The reference's own execution engine on a bounded sample (rank 0 only).
+
+    oracle/_ref/tt_tier2 is the reference's gridjit engine (cuda_launch ->
+    specialize -> lower -> VPTX -> emulated run_kernel, /root/reference/proj/
+    include/gridjit/autolaunch.hpp:167, emulator.hpp:747) compiled from its own
+    headers, running the path written in the reference's kernel DSL
+    (oracle/trace_t05.krn for T0..T5, oracle/circus.krn for the P-functionals
+    of workloads that have them).  It is a separate process that generates its
+    own inputs; nothing of the product package (or any in-tree .so) is loaded
+    here.  Each step runs `threads` angles x `lines` lines of the trace kernel
+    and `crow` circus rows, one DeviceContext per host thread, and reports the
+    launch-only seconds; the step time of the WHOLE workload is extrapolated
+    linearly from those rates (every line / row of the workload costs the same
+    fixed-length loops: n taps twice per line, n samples twice per row)."""
     if rank != 0:
         return None
-    import numpy as np
-
-    import oracle as O
-    import paper_1604_03410_b200 as tt  # noqa: F401 (host inputs only: tables / image)
+    import subprocess
     wl = WORKLOADS[args.workload]
-    n, A = wl["n"], wl["angles"]
-    if not os.path.exists(O.TIER2_PATH):
+    n, A, feats_on = wl["n"], wl["angles"], wl["features"]
+    batch = wl.get("batch", 1)
+    F = 6
+    exe = os.path.join(ROOT, "oracle", "_ref", "tt_tier2")
+    if not os.path.exists(exe):
         return {"impl": "reference", "unavailable": "oracle/_ref/tt_tier2 not built (needs /root/reference)"}
     cores = os.cpu_count() or 1
-    img = tt.synth_image(tt.DISK, n)
-    c, s, w = tt.make_tables(n, A)
-    lines = int(os.environ.get("TT_REF_LINES", "32"))
     threads = min(cores, A)
+    lines = max(1, min(n, int(os.environ.get("TT_REF_LINES", "0")) or 16384 // n))
+    crow = 4 * threads if feats_on else 0
 
     def one():
-        out, med, rep = O.tier2_sample(img, n, c, s, w, angles=threads, lines=lines, threads=threads)
-        return rep
+        r = subprocess.run([exe, "bench", str(n), str(A), str(threads), str(lines), str(crow), str(threads),
+                            os.path.join(ROOT, "oracle", "_ref")], check=True, capture_output=True, text=True)
+        return json.loads(r.stdout.strip().splitlines()[-1])
 
     for _ in range(args.warmup):
         one()
-    times = []
+    steps = []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
         rep = one()
-        times.append(time.perf_counter() - t0)
-    samples = 6 * threads * min(lines, n)
-    t = statistics.mean(times)
+        t_line = rep["trace_seconds"] / rep["trace_lines"]           # s per line on `threads` threads
+        t_row = rep["circus_seconds"] / rep["circus_rows"] if crow else 0.0
+        steps.append((batch * A * n * t_line + (batch * A * F * t_row if feats_on else 0.0), rep))
+    t = statistics.mean(x for x, _ in steps)
+    samples = F * A * n * batch
     value = samples / t
+    rep = steps[-1][1]
+    sample = (f"reference gridjit engine (oracle/_ref/tt_tier2: cuda_launch of oracle/trace_t05.krn"
+              + (" + oracle/circus.krn" if feats_on else "") + f") per step: {threads} angles x {lines} lines "
+              f"x {n} taps" + (f" + {crow} circus rows of {n}" if feats_on else "")
+              + f", one DeviceContext per host thread; launch-only seconds extrapolated to the whole workload "
+              f"({batch} x {A} angles x {n} lines" + (f" + {batch * A * F} circus rows" if feats_on else "") + ")")
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (disk-masked U[0,1) noise, seed 20160412)",
             "config": {"workload": args.workload, "desc": wl["desc"], "image": [n, n], "angles": A,
-                       "functionals": "T0-T5"},
-            "impl": "reference",
+                       "images": batch,
+                       "functionals": "T0-T5" + (" + P1-P3 circus" if feats_on else "")},
+            "impl": "reference", "same_config": True,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"reference gridjit emulator (cuda_launch of oracle/trace_t05.krn) on "
-                                       f"{threads} angles x {lines} lines x {n} taps per step, one DeviceContext "
-                                       f"per host thread"},
+                             "cpu_model": cpu_model(), "nproc": cores, "sample": sample,
+                             "measured_sample_seconds": rep["trace_seconds"] + rep["circus_seconds"],
+                             "extrapolated": True},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(script: str, argv: list, nprocs: int, env=None) -> int:
+    """Re-launch `script argv` as `nprocs` ranks on this node (one process per GPU), the
+    way the driver does: python -m torch.distributed.run --nnodes=1 --nproc-per-node N
+    --master-addr 127.0.0.1 --master-port P.  Rank 0's stdout (the JSON line) passes
+    through; returns the launcher's exit code."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nprocs}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", script, *argv]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -527,16 +629,23 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sampler", type=int, default=int(os.environ.get("TT_BENCH_SAMPLER", "1")), choices=[0, 1])
+    ap.add_argument("--chunks", type=int, default=0, help="angle chunks per shard (orientation sharding; 0: 4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dev-one-gpu", action="store_true",
                     help="validation only: every rank on cuda:0 with gloo (exercises the multi-rank data path, "
                          "incl. the P2P shard writes, on a 1-GPU box; numbers are not a scaling measurement)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # plain `python bench.py --gpus N`: spawn the N ranks ourselves
+        sys.exit(spawn_ranks(os.path.abspath(__file__), sys.argv[1:], args.gpus))
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        sys.exit(2)
     line = run_reference(args, ws, rank) if args.impl == "reference" else run_ours(args, ws, rank, local)
     if line is not None and rank == 0:
         print(json.dumps(line), flush=True)

@@ -363,6 +363,10 @@ typedef struct tt_plan_desc {
                          0 = automatic */
     int32_t slots;    /* device buffer sets for overlapping submissions (1..4; 0: 2 for one
                          image, 1 for batches) */
+    int32_t pair_stride; /* 0: the drop-in pairing over [a0, a0+a_count) (tt_trace_desc rule);
+                            > 0: an orientation shard with its mirror half -- a_count even, the
+                            angles a0+i and a0+i+pair_stride for i < a_count/2, output rows
+                            [a_count/2] + [a_count/2] (shard.orientation_shard: pair_stride = A/2) */
 } tt_plan_desc;
 tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out);
 /* h_img [batch][n][n]; h_out [batch][a_count][F][n], h_med [batch][a_count][2][n],

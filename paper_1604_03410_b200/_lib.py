@@ -50,7 +50,7 @@ class Counters(C.Structure):
 
 class PlanDesc(C.Structure):
     _fields_ = [(k, C.c_int32) for k in ("n", "a_total", "a0", "a_count", "full", "features", "batch", "chunks",
-                                         "slots")]
+                                         "slots", "pair_stride")]
 
 
 class TraceDesc(C.Structure):

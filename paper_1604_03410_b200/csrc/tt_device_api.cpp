@@ -305,13 +305,21 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
         return fail(ctx, TT_ERR_INVALID, "bad plan descriptor");
     if ((long long)d->a_count * n * (d->batch > 1 ? d->batch : 1) >= (1ll << 31))
         return fail(ctx, TT_ERR_INVALID, "plan too large");
+    if (d->pair_stride < 0 ||
+        (d->pair_stride > 0 && (d->a_count % 2 != 0 || d->a0 + d->a_count / 2 + d->pair_stride > d->a_total)))
+        return fail(ctx, TT_ERR_INVALID, "explicit pair_stride needs an even a_count inside the angle grid");
     DeviceGuard guard(ctx->device);
     auto p = new tt_plan;
     p->ctx = ctx;
     p->d = *d;
     p->d.batch = d->batch > 1 ? d->batch : 1;
     p->F = d->full ? tt::kNumF : 1;
-    tt::launch_structure(d->a_count, &p->units, &p->pair);
+    if (d->pair_stride > 0) {  // orientation shard + mirror half: rows [units] + [units]
+        p->units = d->a_count / 2;
+        p->pair = d->pair_stride;
+    } else {
+        tt::launch_structure(d->a_count, &p->units, &p->pair);
+    }
     const int B = p->d.batch;
     // chunks: >= ~1.6e7 unit-taps (~40 us of kernel) each so the per-chunk enqueue cost stays hidden,
     // at most 32 (measured on C2: 5 chunks 1.28 ms, 24-32 chunks 1.24 ms; C1 best unchunked)

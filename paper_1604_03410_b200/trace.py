@@ -190,11 +190,12 @@ class Plan:
 
     def __init__(self, ctx: DeviceContext, n: int, angles: int, full: bool = True, a0: int = 0,
                  a_count: int | None = None, features: bool = False, batch: int = 1, chunks: int = 0,
-                 slots: int = 0):
+                 slots: int = 0, pair_stride: int = 0):
         self.ctx, self.n, self.full, self.batch = ctx, n, full, batch
         self.a_count = angles - a0 if a_count is None else a_count
         self.features = features and full
-        d = _lib.PlanDesc(n, angles, a0, self.a_count, int(full), int(self.features), batch, chunks, slots)
+        d = _lib.PlanDesc(n, angles, a0, self.a_count, int(full), int(self.features), batch, chunks, slots,
+                          pair_stride)
         self._p = C.c_void_p()
         _check(lib.tt_plan_create(ctx._p, C.byref(d), C.byref(self._p)), ctx._p)
         c = C.c_int()

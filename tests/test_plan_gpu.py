@@ -53,6 +53,29 @@ def test_plan_angle_range_and_partial_outputs(ctx):
     plan.destroy()
 
 
+@pytest.mark.parametrize("world,rank", [(2, 0), (2, 1), (4, 3), (3, 1)])
+def test_plan_mirror_half_shard_equals_rows_of_the_whole(ctx, world, rank):
+    """An orientation shard with its mirror half (pair_stride = A/2): rows [cnt] + [cnt] equal the
+    corresponding rows (a0.., A/2+a0..) of the whole transform, bit for bit."""
+    from paper_1604_03410_b200 import shard
+    ctx.set_sampler(1)
+    n, A = 256, 40
+    img = tt.synth_image(tt.PHANTOM, n)
+    whole, wmed, _ = tt.TraceTransform(ctx, n, A)(img)
+    a0, cnt, h = shard.orientation_shard(A, world, rank)
+    plan = tt.Plan(ctx, n, A, a0=a0, a_count=2 * cnt, pair_stride=h, chunks=3)
+    out = np.full((2 * cnt, NF, n), np.nan, np.float32)
+    med = np.full((2 * cnt, 2, n), -1, np.int32)
+    plan.run(img, out, med)
+    rows = shard.shard_rows(A, world, rank)
+    assert np.array_equal(_bits(out), _bits(whole[rows])) and np.array_equal(med, wmed[rows])
+    plan.destroy()
+    with pytest.raises(tt.Error):  # odd a_count / partner angles outside the grid
+        tt.Plan(ctx, n, A, a0=a0, a_count=3, pair_stride=h)
+    with pytest.raises(tt.Error):
+        tt.Plan(ctx, n, A, a0=h, a_count=2 * cnt, pair_stride=h)
+
+
 @pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
 @pytest.mark.parametrize("chunks", [0, 2, 3])
 def test_plan_batched_features(ctx, chunks, sampler):
