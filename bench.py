@@ -298,17 +298,20 @@ def run_ours(args, ws, rank, local):
             tex = image_atlas(img.data_ptr(), n, B, 0, sptr) if B > 1 else image_texture(img.data_ptr(), n, sptr)
         if full:
             tt.weights_soa(wtab.data_ptr(), n, wsoa.data_ptr(), sptr)
-        launches_per_step = 1 + (1 if feats_on else 0) + (1 if tex is not None and B > 1 else 0)
+        # the P stage runs as the trace kernel's epilogue (TT_FUSED_CIRCUS=0: a separate circus launch)
+        fused = feats_on and os.environ.get("TT_FUSED_CIRCUS", "1") != "0"
+        launches_per_step = 1 + (1 if feats_on and not fused else 0) + (1 if tex is not None and B > 1 else 0)
 
         def step():
             if tex is not None:
                 image_texture_update(tex, img.data_ptr(), 0, sptr)
             tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
                             out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
-                            pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0)
+                            pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0,
+                            circ_ptr=circ.data_ptr() if fused else 0)
 
         def features():
-            if feats_on:  # P-functional (circus) stage consuming the sinograms
+            if feats_on and not fused:  # P-functional (circus) stage consuming the sinograms
                 tt.circus_device(out.data_ptr(), n, B * a_cnt * F, circ.data_ptr(), stream=sptr)
             if dist:      # image sharding: gather the per-image circus features
                 with torch.cuda.stream(stream):

@@ -275,6 +275,9 @@ typedef struct tt_trace_desc {
                             out + a0 rows and partner_row = A/2 (batch 1). */
     int32_t flags;       /* TT_TRACE_PEER_OUT: out/med are another GPU's memory (IPC / NVLink):
                             each thread fences its stores at system scope before it exits */
+    float* circ;         /* optional (full only): the P stage fused into the launch -- circ[row][6][3]
+                            = tt_circus_device over the launch's sinogram rows, computed by the
+                            group that finishes each unit's last line (bit-identical); NULL: none */
 } tt_trace_desc;
 #define TT_TRACE_PEER_OUT 1
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream);

@@ -58,7 +58,7 @@ class TraceDesc(C.Structure):
                 ("full", C.c_int32), ("ctab", C.c_void_p), ("stab", C.c_void_p), ("wtab", C.c_void_p),
                 ("out", C.c_void_p), ("med", C.c_void_p), ("sampler", C.c_int32), ("pair_stride", C.c_int32),
                 ("batch", C.c_int32), ("_pad2", C.c_int32), ("img_stride", C.c_int64), ("wsoa", C.c_void_p),
-                ("partner_row", C.c_int32), ("flags", C.c_int32)]
+                ("partner_row", C.c_int32), ("flags", C.c_int32), ("circ", C.c_void_p)]
 
 
 class IpcHandle(C.Structure):

@@ -3,6 +3,7 @@
 // host-to-host plans (tt_plan_*) and the inter-process pointers (tt_ipc_*).
 // Shares the context internals of tt_context_impl.h.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -78,6 +79,7 @@ static tt::TraceArgs to_args(const tt_trace_desc* d) {
     ta.full = d->full != 0;
     ta.batch = d->batch > 1 ? d->batch : 1;
     ta.img_stride = d->img_stride;
+    ta.circ = d->full ? d->circ : nullptr;
     return ta;
 }
 
@@ -99,6 +101,24 @@ struct WeightScratch {
     }
 };
 
+// Per-unit line counters of the fused P stage for one raw launch (stream-ordered scratch).
+struct CounterScratch {
+    int* d = nullptr;
+    cudaStream_t s = nullptr;
+    ~CounterScratch() {
+        if (d) cudaFreeAsync(d, s);
+    }
+    cudaError_t prepare(tt::TraceArgs& ta, cudaStream_t stream) {
+        if (!ta.circ) return cudaSuccess;
+        s = stream;
+        const std::size_t bytes = std::size_t(ta.batch) * ta.a_count * sizeof(int);
+        cudaError_t e = cudaMallocAsync((void**)&d, bytes ? bytes : 4, stream);
+        if (e != cudaSuccess) return e;
+        ta.unit_done = d;
+        return cudaMemsetAsync(d, 0, bytes, stream);
+    }
+};
+
 tt_status tt_weights_soa(const float* d_wtab, int n, float* d_wsoa, void* stream) {
     if (!d_wtab || !d_wsoa || n < 1) return fail(nullptr, TT_ERR_INVALID, "bad weight-table arguments");
     if ((reinterpret_cast<std::uintptr_t>(d_wtab) | reinterpret_cast<std::uintptr_t>(d_wsoa)) & 15u)
@@ -115,6 +135,8 @@ tt_status tt_trace_device(const tt_trace_desc* d, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     WeightScratch ws;
     if (cudaError_t e = ws.prepare(ta, s); e != cudaSuccess) return cuda_fail(nullptr, e, "weight table");
+    CounterScratch cs;
+    if (cudaError_t e = cs.prepare(ta, s); e != cudaSuccess) return cuda_fail(nullptr, e, "circus counters");
     if (d->sampler == 1) {
         cudaArray_t arr = nullptr;
         ta.sampler = tt::Sampler::Texture;
@@ -220,6 +242,9 @@ tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, voi
     WeightScratch ws;
     if (cudaError_t e = ws.prepare(ta, (cudaStream_t)stream); e != cudaSuccess)
         return cuda_fail(nullptr, e, "weight table");
+    CounterScratch cs;
+    if (cudaError_t e = cs.prepare(ta, (cudaStream_t)stream); e != cudaSuccess)
+        return cuda_fail(nullptr, e, "circus counters");
     cudaError_t e = tt::launch_trace(ta, (cudaStream_t)stream);
     return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "trace kernel");
 }
@@ -247,6 +272,7 @@ struct PlanSlot {
     float* img = nullptr;  // linear image(s) (LDG sampler, batched atlas fill)
     float *out = nullptr, *circ = nullptr;
     std::int32_t* med = nullptr;
+    int* unit_done = nullptr;  // fused P stage: per-unit line counters (zeroed once, self-resetting)
     cudaArray_t arr = nullptr;
     cudaTextureObject_t tex = 0;
     std::vector<cudaEvent_t> done;      // per chunk: its rows are final
@@ -260,6 +286,7 @@ struct tt_plan {
     tt_ctx* ctx = nullptr;
     tt_plan_desc d{};
     int F = 1, units = 0, pair = 0, chunks = 1, cols = 1, next = 0;
+    bool fused_circus = true;  // P stage as the trace kernel's epilogue (TT_FUSED_CIRCUS=0: separate launch)
     float *ctab = nullptr, *stab = nullptr, *wtab = nullptr, *wsoa = nullptr;
     std::vector<PlanSlot> slot;
     cudaStream_t sc[2] = {nullptr, nullptr}, sx = nullptr, si = nullptr;
@@ -280,7 +307,7 @@ void plan_release(tt_plan* p) {
             if (e) cudaEventDestroy(e);
         if (sl.tex) cudaDestroyTextureObject(sl.tex);
         if (sl.arr) cudaFreeArray(sl.arr);
-        for (void* b : {(void*)sl.img, (void*)sl.out, (void*)sl.circ, (void*)sl.med})
+        for (void* b : {(void*)sl.img, (void*)sl.out, (void*)sl.circ, (void*)sl.med, (void*)sl.unit_done})
             if (b) cudaFree(b);
     }
     for (void* b : {(void*)p->ctab, (void*)p->stab, (void*)p->wtab, (void*)p->wsoa})
@@ -314,6 +341,7 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
     p->d = *d;
     p->d.batch = d->batch > 1 ? d->batch : 1;
     p->F = d->full ? tt::kNumF : 1;
+    if (const char* fc = std::getenv("TT_FUSED_CIRCUS")) p->fused_circus = std::atoi(fc) != 0;
     if (d->pair_stride > 0) {  // orientation shard + mirror half: rows [units] + [units]
         p->units = d->a_count / 2;
         p->pair = d->pair_stride;
@@ -347,7 +375,11 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
         alloc(&sl.img, B * N2 * 4);
         alloc(&sl.out, rows * p->F * n * 4);
         if (d->full) alloc(&sl.med, rows * 2 * n * 4);
-        if (d->features) alloc(&sl.circ, rows * tt::kNumF * 3 * 4);
+        if (d->features) {
+            alloc(&sl.circ, rows * tt::kNumF * 3 * 4);
+            alloc(&sl.unit_done, std::size_t(B) * p->units * 4);
+            if (e == cudaSuccess) e = cudaMemsetAsync(sl.unit_done, 0, std::size_t(B) * p->units * 4, p->sc[0]);
+        }
         sl.done.resize(p->chunks, nullptr);
         sl.uploaded.resize(p->chunks, nullptr);
         for (auto* evs : {&sl.done, &sl.uploaded})
@@ -424,6 +456,10 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
         ta.full = d.full != 0;
         ta.batch = b1 - b0;
         ta.img0 = b0;
+        if (d.features && p->fused_circus) {  // fused P stage: the rows' circus features, per-unit counters
+            ta.circ = sl.circ + rows0 * row_c;
+            ta.unit_done = sl.unit_done + std::size_t(b0) * p->units + u0;
+        }
         return ta;
     };
     auto download = [&](std::size_t r0, std::size_t cnt) {  // output rows [r0, r0 + cnt) on the copy stream
@@ -460,10 +496,12 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
             if (h_out || h_med)
                 for (int half = 0; half < (p->pair ? 2 : 1); ++half) download(std::size_t(u0 + half * p->units), u1 - u0);
         }
-        if (d.features) {  // 3. P-functionals over the whole sinogram
+        if (d.features) {  // 3. P-functionals over the whole sinogram (fused: computed by the trace launches)
             const std::size_t rows = d.a_count;
-            ok(tt::launch_circus(sl.out, n, int(rows * tt::kNumF), sl.circ, p->sx));
-            ++launches;
+            if (!p->fused_circus) {
+                ok(tt::launch_circus(sl.out, n, int(rows * tt::kNumF), sl.circ, p->sx));
+                ++launches;
+            }
             if (h_circ) {
                 ok(cudaMemcpyAsync(h_circ, sl.circ, rows * row_c * 4, cudaMemcpyDeviceToHost, p->sx));
                 d2h += rows * row_c * 4;
@@ -489,7 +527,7 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
             if (!ok(tt::launch_trace(ta, s))) break;
             launches += tt::trace_launch_count(ta);
             const std::size_t r0 = std::size_t(b0) * units_all, rows = cnt * units_all;
-            if (d.features) {
+            if (d.features && !p->fused_circus) {
                 ok(tt::launch_circus(sl.out + r0 * row_f, n, int(rows * tt::kNumF), sl.circ + r0 * row_c, s));
                 ++launches;
             }

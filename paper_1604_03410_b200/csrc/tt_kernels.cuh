@@ -43,6 +43,8 @@ struct TraceArgs {
     int img0 = 0;                 // atlas/array index of the launch's first image (outputs stay launch-relative)
     long long img_stride = 0;     // elements between images (0: n*n) -- Global sampler
     int atlas_cols = 1;           // texture atlas tiles per row -- Texture sampler
+    float* circ = nullptr;        // full: fused P stage -- [rows][6][3] circus features of the launch's rows
+    int* unit_done = nullptr;     // with circ: [batch * a_count] zeroed line counters (left zeroed)
 };
 
 // Slots (lanes) per line of the fused kernel for side n: 8/16/32 (one warp

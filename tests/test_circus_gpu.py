@@ -68,3 +68,38 @@ def test_resident_flow_with_features(ctx):
     assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
     rc, _, _ = O.circus(out)
     assert np.array_equal(circ.view(np.uint32), rc.view(np.uint32))
+
+
+@pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
+@pytest.mark.parametrize("n,A,batch,pair", [(64, 10, 1, 0), (128, 9, 1, 0), (256, 12, 3, 0), (1024, 8, 1, 0),
+                                            (1000, 6, 1, 0), (2048, 4, 1, 0), (4096, 2, 1, 0), (256, 16, 1, 8),
+                                            (256, 16, 1, 4)])
+def test_fused_circus_epilogue_equals_separate_stage(gpu, n, A, batch, pair, sampler):
+    """tt_trace_desc.circ: the P stage as the trace kernel's epilogue (the group finishing a unit's
+    last line computes its rows) -- bit-identical to tt_circus_device over the same rows, and to the
+    oracle's replay; covers sub-warp segments, W > 1 warps per line, batches, unpaired units and
+    explicit mirror-half shards."""
+    import torch
+    c, s, w = tt.make_tables(n, A)
+    imgs = np.stack([tt.synth_image(tt.PHANTOM, n, 7 + b) for b in range(batch)])
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    img, ct, st, wt = dev(imgs), dev(c), dev(s), dev(w)
+    a_count = A if pair == 0 else 2 * (A // 4)
+    out = torch.empty((batch, a_count, 6, n), device="cuda")
+    med = torch.empty((batch, a_count, 2, n), dtype=torch.int32, device="cuda")
+    circ = torch.full((batch, a_count, 6, 3), float("nan"), device="cuda")
+    tex = None
+    if sampler == 1:
+        tex = tt.trace.image_atlas(img.data_ptr(), n, batch) if batch > 1 else tt.trace.image_texture(img.data_ptr(), n)
+    for _ in range(2):  # the per-unit counters reset themselves: a second launch must work the same
+        tt.trace_device(img.data_ptr(), n, 0, a_count, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
+                        med.data_ptr(), sampler=sampler, tex=tex, batch=batch, pair_stride=pair,
+                        circ_ptr=circ.data_ptr())
+    ref = torch.empty_like(circ)
+    tt.circus_device(out.data_ptr(), n, batch * a_count * 6, ref.data_ptr())
+    torch.cuda.synchronize()
+    if tex is not None:
+        tt.trace.image_texture_destroy(tex)
+    got = circ.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), ref.cpu().numpy().view(np.uint32))
+    _check_against_truth(out.cpu().numpy(), got)
