@@ -428,10 +428,11 @@ namespace b200 {
 class TracePlan {
   public:
     TracePlan(DeviceContext& ctx, int n, int angles, bool full = true, bool features = false, int a0 = 0,
-              int a_count = -1, int batch = 1, int chunks = 0, int slots = 0, int pair_stride = 0)
+              int a_count = -1, int batch = 1, int chunks = 0, int slots = 0, int pair_stride = 0,
+              bool graph = false)
         : ctx_(ctx.raw()) {
         tt_plan_desc d{n, angles, a0, a_count < 0 ? angles - a0 : a_count, full ? 1 : 0, features ? 1 : 0,
-                       batch, chunks, slots, pair_stride};
+                       batch, chunks, slots, pair_stride, graph ? 1 : 0};
         detail::check(tt_plan_create(ctx_, &d, &p_), ctx_);
     }
     TracePlan(const TracePlan&) = delete;

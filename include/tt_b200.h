@@ -240,12 +240,12 @@ tt_status tt_tld4_probe(unsigned* d_out, int blocks, int iters, void* stream);
 /* Raw device-pointer entry (multi-GPU driver, benchmarks): enqueue the fused
  * kernel for a_count angles on `stream` (cudaStream_t; NULL = legacy
  * default).  out: full ? [a_count][6][n] : [a_count][n]; med may be NULL.
- * sampler: 0 = global/L1 loads (asynchronous: the call only enqueues), 1 =
- * texture gather through a cudaArray copy of img that this call makes and
- * releases -- which makes sampler 1 SYNCHRONOUS (the call waits for the
- * launch before freeing the copy).  Asynchronous texture launches go through
- * tt_image_tex_create + tt_trace_device_tex (the copy outlives the call);
- * that is what the plans and the multi-GPU driver use.
+ * sampler: 0 = global/L1 loads, 1 = texture gather through a cudaArray copy of
+ * img that this call makes; both are asynchronous (the call only enqueues):
+ * the copy is released once its launch has completed (recorded event, reclaimed
+ * by later calls and at exit).  Repeated texture launches on one image should
+ * use tt_image_tex_create + tt_trace_device_tex (one copy for all of them);
+ * that is what the plans and the multi-GPU driver do.
  * pair_stride: 0 = the drop-in rule (angles [a0, a0+a_count); pairs
  * (a0+i, a0+i+a_count/2) when a_count is even); -1 = no pairing; > 0 = the
  * angles are a0+i and a0+i+pair_stride for i < a_count/2 (rows i and
@@ -316,6 +316,23 @@ tt_status tt_circus_device(const float* d_sino, int n, int rows, float* d_circ, 
  * no trace-transform code); it sits beside tt_circus_device. */
 tt_status tt_circus_fft_device(const float* d_sino, int n, int rows, double* d_p, void* stream);
 
+/* Hermite P-functionals (the Hermite circus functionals of
+ * the cited prior work, PAPER.md:813,817 -- no reference interface exists):
+ * for each of `rows` sinogram rows of length n, with centre c = the row's
+ * weighted median index (the P2 index of tt_circus_device, bit-identical),
+ * d_hp[row][k] = sum_p s_p psi_k(z_p) for k < orders (1..8), psi_k the
+ * normalised Hermite functions and z_p = (p-c)*10/c below the centre,
+ * (p-c)*10/(n-1-c) above it; f64.  d_center[row] = c (may be NULL). */
+tt_status tt_hermite_device(const float* d_sino, int n, int rows, int orders, double* d_hp, int32_t* d_center,
+                            void* stream);
+/* Orthonormal (square) sinogram input: the h x w image on
+ * device resampled bilinearly to s x s, s = tt_orthonormal_side(angles) =
+ * ceil(angles / sqrt 2), and centred in an angles x angles frame (d_out), so
+ * that the trace transform of d_out over `angles` orientations is square
+ * (angles lines per orientation). */
+int tt_orthonormal_side(int angles);
+tt_status tt_orthonormal_device(const float* d_img, int h, int w, int angles, float* d_out, void* stream);
+
 /* Prepared texture for repeated tt_trace_device calls on one image
  * (sampler 1 without the per-call copy). */
 typedef struct tt_image_tex tt_image_tex;
@@ -370,6 +387,9 @@ typedef struct tt_plan_desc {
                             > 0: an orientation shard with its mirror half -- a_count even, the
                             angles a0+i and a0+i+pair_stride for i < a_count/2, output rows
                             [a_count/2] + [a_count/2] (shard.orientation_shard: pair_stride = A/2) */
+    int32_t graph;       /* 1: capture each slot's submission into a CUDA graph (per set of host
+                            buffers) and replay it -- one host call per submit (the latency path for
+                            small images, C1); 0: enqueue the calls every time */
 } tt_plan_desc;
 tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out);
 /* h_img [batch][n][n]; h_out [batch][a_count][F][n], h_med [batch][a_count][2][n],
@@ -382,6 +402,8 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, int32_t* h_m
 tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, int32_t* h_med, float* h_circ);
 tt_status tt_plan_wait(tt_plan* p);
 tt_status tt_plan_chunks(const tt_plan* p, int* chunks);
+/* Graph mode: submissions captured so far (one per slot and host-buffer set; the rest replayed). */
+tt_status tt_plan_captures(const tt_plan* p, int* captures);
 tt_status tt_plan_destroy(tt_plan* p);
 
 #ifdef __cplusplus

@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import math
 import os
 import subprocess
 import tempfile
@@ -67,6 +68,9 @@ def lib():
         L.tto_check_lines.argtypes = [fp, ctypes.c_int, fp, fp, fp, ctypes.c_int, ctypes.c_int, ip, ip, fp, ip,
                                       ctypes.c_double, ctypes.c_int, ctypes.c_double, dp, ctypes.c_int]
         L.tto_check_lines.restype = ctypes.c_long
+        L.tto_orthonormal_side.argtypes = [ctypes.c_int]
+        L.tto_orthonormal_side.restype = ctypes.c_int
+        L.tto_orthonormal.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp]
         _lib = L
     return _lib
 
@@ -256,3 +260,43 @@ def prep(pix, n: int):
     y0, x0 = (n - h) // 2, (n - w) // 2
     out[y0:y0 + h, x0:x0 + w] = v
     return out
+
+
+def orthonormal(img, angles: int):
+    """CPU restatement of tt_orthonormal_device: bit-exact f32 frame [A][A]."""
+    img = np.ascontiguousarray(img, np.float32)
+    h, w = img.shape
+    out = np.empty((angles, angles), np.float32)
+    lib().tto_orthonormal(_f(img), h, w, angles, _f(out))
+    return out
+
+
+def orthonormal_side(angles: int) -> int:
+    return lib().tto_orthonormal_side(angles)
+
+
+def hermite(sino, center, orders: int):
+    """Hermite P-functionals in f64 around the given per-row centres:
+    returns (H f64 [..., orders], M f64 [..., orders] = sum_p |s_p psi_k(z_p)|, the scale of the
+    rounding error).  psi_k(z) = h_k(z) exp(-z^2/2) / sqrt(2^k k! sqrt(pi)), h_k the physicists'
+    Hermite polynomials; z_p = (p - c) * 10 / c below the centre, (p - c) * 10 / (n - 1 - c) above."""
+    s = np.asarray(sino, np.float64)
+    n = s.shape[-1]
+    rows = s.reshape(-1, n)
+    c = np.asarray(center, np.int64).reshape(-1)
+    p = np.arange(n)[None, :]
+    lo = np.where(c > 0, 10.0 / np.maximum(c, 1), 0.0)[:, None]
+    hi = np.where(c < n - 1, 10.0 / np.maximum(n - 1 - c, 1), 0.0)[:, None]
+    z = (p - c[:, None]) * np.where(p < c[:, None], lo, hi)
+    e = np.exp(-0.5 * z * z)
+    H = np.empty((rows.shape[0], orders))
+    M = np.empty((rows.shape[0], orders))
+    h0, h1 = np.ones_like(z), 2.0 * z
+    for k in range(orders):
+        norm = 1.0 / np.sqrt(2.0 ** k * math.factorial(k) * np.sqrt(np.pi))
+        t = rows * e * norm * h0
+        H[:, k] = t.sum(axis=1)
+        M[:, k] = np.abs(t).sum(axis=1)
+        h0, h1 = h1, 2.0 * z * h1 - 2.0 * (k + 1) * h0
+    shp = s.shape[:-1] + (orders,)
+    return H.reshape(shp), M.reshape(shp)

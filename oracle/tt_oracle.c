@@ -824,3 +824,34 @@ long tto_check_lines(const float* img, int n, const float* ctab, const float* st
     }
     return fails;
 }
+
+/* ---------------------------------------------------- orthonormal frame */
+/* the h x w image resampled bilinearly to s x s (s = ceil(A / sqrt 2)), centred in
+ * an A x A frame; src = (dst + 0.5) * (w / s) - 0.5 clamped to [0, w-1], the sampler's bilinear form.
+ * Restates tt_kernels.cu orthonormal_kernel. */
+int tto_orthonormal_side(int angles) { return angles < 1 ? 0 : (int)ceil(angles / sqrt(2.0)); }
+
+void tto_orthonormal(const float* img, int h, int w, int A, float* out) {
+    const int s = tto_orthonormal_side(A), off = (A - s) / 2;
+    const float sx = (float)w / (float)s, sy = (float)h / (float)s;
+    for (int yy = 0; yy < A; ++yy)
+        for (int xx = 0; xx < A; ++xx) {
+            const int y = yy - off, x = xx - off;
+            float v = 0.0f;
+            if (x >= 0 && x < s && y >= 0 && y < s) {
+                float fx = ((float)x + 0.5f) * sx - 0.5f;
+                float fy = ((float)y + 0.5f) * sy - 0.5f;
+                fx = fminf(fmaxf(fx, 0.0f), (float)(w - 1));
+                fy = fminf(fmaxf(fy, 0.0f), (float)(h - 1));
+                const int x0 = (int)fx, y0 = (int)fy;
+                const int x1 = x0 + 1 < w ? x0 + 1 : w - 1, y1 = y0 + 1 < h ? y0 + 1 : h - 1;
+                const float ax = fx - (float)x0, ay = fy - (float)y0;
+                const float i00 = img[(size_t)y0 * w + x0], i01 = img[(size_t)y0 * w + x1];
+                const float i10 = img[(size_t)y1 * w + x0], i11 = img[(size_t)y1 * w + x1];
+                const float top = fmaf(ax, i01 - i00, i00);
+                const float bot = fmaf(ax, i11 - i10, i10);
+                v = fmaf(ay, bot - top, top);
+            }
+            out[(size_t)yy * A + xx] = v;
+        }
+}

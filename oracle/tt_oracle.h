@@ -40,6 +40,10 @@
 
 #ifdef __cplusplus
 extern "C" {
+/* Orthonormal (square) sinogram input frame, DESIGN.md §2.8 (restates tt_orthonormal_device). */
+int tto_orthonormal_side(int angles);
+void tto_orthonormal(const float* img, int h, int w, int angles, float* out);
+
 #endif
 
 enum { TTO_F64 = 0, TTO_SEQ32 = 1, TTO_REPLAY = 2 };
@@ -131,5 +135,13 @@ long tto_check_lines(const float* img, int n, const float* ctab, const float* st
 
 #ifdef __cplusplus
 }
+/* Orthonormal (square) sinogram input frame, DESIGN.md §2.8 (restates tt_orthonormal_device). */
+int tto_orthonormal_side(int angles);
+void tto_orthonormal(const float* img, int h, int w, int angles, float* out);
+
 #endif
+/* Orthonormal (square) sinogram input frame, DESIGN.md §2.8 (restates tt_orthonormal_device). */
+int tto_orthonormal_side(int angles);
+void tto_orthonormal(const float* img, int h, int w, int angles, float* out);
+
 #endif

@@ -23,4 +23,5 @@ from .api import (  # noqa: F401
 from .trace import (  # noqa: F401
     CIRCUS, CIRCUS_FFT, DISK, PHANTOM, SEEDS, SPARSE, Plan, TRACE_T05, TRACE_T05_BATCH, RADON, TraceTransform, circus, circus_device, circus_fft, circus_fft_device, make_tables,
     ipc_close, ipc_export, ipc_import, max_full_n, prep_device, prep_side, read_pnm, write_pgm, schedule_slots, synth_image, trace_device, weights_soa,
+    HERMITE, ORTHONORMAL, hermite, hermite_device, orthonormal_device, orthonormal_image, orthonormal_side,
 )

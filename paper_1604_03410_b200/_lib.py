@@ -50,7 +50,7 @@ class Counters(C.Structure):
 
 class PlanDesc(C.Structure):
     _fields_ = [(k, C.c_int32) for k in ("n", "a_total", "a0", "a_count", "full", "features", "batch", "chunks",
-                                         "slots", "pair_stride")]
+                                         "slots", "pair_stride", "graph")]
 
 
 class TraceDesc(C.Structure):
@@ -123,11 +123,15 @@ _sigs = {
     "tt_trace_device_tex": (_S, [C.POINTER(TraceDesc), C.c_void_p, C.c_void_p]),
     "tt_jit_source": (_S, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "tt_vptx_body_fingerprint": (_S, [C.c_char_p, C.c_size_t, C.c_char_p, C.POINTER(C.c_uint64)]),
+    "tt_hermite_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tt_orthonormal_side": (C.c_int, [C.c_int]),
+    "tt_orthonormal_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_plan_create": (_S, [C.c_void_p, C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]),
     "tt_plan_run": (_S, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tt_plan_submit": (_S, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tt_plan_wait": (_S, [C.c_void_p]),
     "tt_plan_chunks": (_S, [C.c_void_p, C.POINTER(C.c_int)]),
+    "tt_plan_captures": (_S, [C.c_void_p, C.POINTER(C.c_int)]),
     "tt_plan_destroy": (_S, [C.c_void_p]),
 }
 for _name, (_res, _args) in _sigs.items():

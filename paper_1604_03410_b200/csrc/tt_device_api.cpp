@@ -3,6 +3,7 @@
 // host-to-host plans (tt_plan_*) and the inter-process pointers (tt_ipc_*).
 // Shares the context internals of tt_context_impl.h.
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -11,10 +12,57 @@
 #include <vector>
 
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "tt_context_impl.h"
 
 using namespace ttc;
+
+namespace {
+
+// Texture copies made by tt_trace_device (sampler 1) for one launch: released once the launch has
+// completed (its event), by later calls or at exit -- the call itself never blocks the host.
+struct DeferredTex {
+    cudaArray_t arr = nullptr;
+    cudaTextureObject_t tex = 0;
+    cudaEvent_t done = nullptr;
+    int device = 0;
+};
+std::mutex g_tex_mu;
+std::vector<DeferredTex> g_tex_pending;
+
+void release(const DeferredTex& t) {
+    DeviceGuard guard(t.device);
+    cudaDestroyTextureObject(t.tex);
+    cudaFreeArray(t.arr);
+    cudaEventDestroy(t.done);
+}
+
+void reclaim_textures(bool all) {
+    std::lock_guard<std::mutex> lk(g_tex_mu);
+    auto it = g_tex_pending.begin();
+    while (it != g_tex_pending.end()) {
+        if (all) cudaEventSynchronize(it->done);
+        if (all || cudaEventQuery(it->done) == cudaSuccess) {
+            release(*it);
+            it = g_tex_pending.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+struct TexReaper {
+    ~TexReaper() { reclaim_textures(true); }
+} g_tex_reaper;
+
+// NVTX range (nvtx3, header-only: a no-op unless a profiler injects itself).
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+};
+
+}  // namespace
 
 extern "C" {
 
@@ -101,7 +149,7 @@ struct WeightScratch {
     }
 };
 
-// Per-unit line counters of the fused P stage for one raw launch (stream-ordered scratch).
+// State of the fused P stage for one raw launch (stream-ordered scratch).
 struct CounterScratch {
     int* d = nullptr;
     cudaStream_t s = nullptr;
@@ -111,10 +159,10 @@ struct CounterScratch {
     cudaError_t prepare(tt::TraceArgs& ta, cudaStream_t stream) {
         if (!ta.circ) return cudaSuccess;
         s = stream;
-        const std::size_t bytes = std::size_t(ta.batch) * ta.a_count * sizeof(int);
-        cudaError_t e = cudaMallocAsync((void**)&d, bytes ? bytes : 4, stream);
+        const std::size_t bytes = tt::epi_state_ints(ta) * sizeof(int);
+        cudaError_t e = cudaMallocAsync((void**)&d, bytes, stream);
         if (e != cudaSuccess) return e;
-        ta.unit_done = d;
+        ta.epi = d;
         return cudaMemsetAsync(d, 0, bytes, stream);
     }
 };
@@ -128,6 +176,7 @@ tt_status tt_weights_soa(const float* d_wtab, int n, float* d_wsoa, void* stream
 }
 
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream) {
+    Range r("tt_trace_device");
     tt_status st = check_desc(d);
     if (st != TT_OK) return st;
     if (!d->img) return fail(nullptr, TT_ERR_INVALID, "null image");
@@ -138,18 +187,27 @@ tt_status tt_trace_device(const tt_trace_desc* d, void* stream) {
     CounterScratch cs;
     if (cudaError_t e = cs.prepare(ta, s); e != cudaSuccess) return cuda_fail(nullptr, e, "circus counters");
     if (d->sampler == 1) {
-        cudaArray_t arr = nullptr;
+        reclaim_textures(false);  // copies of earlier calls whose launches have completed
+        DeferredTex t;
+        cudaGetDevice(&t.device);
         ta.sampler = tt::Sampler::Texture;
         cudaError_t e = ta.batch > 1
                             ? tt::make_image_atlas(ta.img, ta.n, ta.batch, ta.img_stride > 0 ? ta.img_stride
                                                                                            : (long long)ta.n * ta.n,
-                                                   s, &arr, &ta.tex, &ta.atlas_cols)
-                            : tt::make_image_texture(ta.img, ta.n, s, &arr, &ta.tex);
-        if (e != cudaSuccess) return cuda_fail(nullptr, e, "image texture");
-        e = tt::launch_trace(ta, s);
-        cudaStreamSynchronize(s);
-        cudaDestroyTextureObject(ta.tex);
-        cudaFreeArray(arr);
+                                                   s, &t.arr, &ta.tex, &ta.atlas_cols)
+                            : tt::make_image_texture(ta.img, ta.n, s, &t.arr, &ta.tex);
+        t.tex = ta.tex;
+        if (e == cudaSuccess) e = tt::launch_trace(ta, s);
+        const cudaError_t ev = cudaEventCreateWithFlags(&t.done, cudaEventDisableTiming);
+        if (ev == cudaSuccess && cudaEventRecord(t.done, s) == cudaSuccess) {
+            std::lock_guard<std::mutex> lk(g_tex_mu);
+            g_tex_pending.push_back(t);  // released once the launch has completed
+        } else {  // no event: fall back to waiting here
+            cudaStreamSynchronize(s);
+            if (t.tex) cudaDestroyTextureObject(t.tex);
+            if (t.arr) cudaFreeArray(t.arr);
+            if (t.done) cudaEventDestroy(t.done);
+        }
         return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "trace kernel");
     }
     cudaError_t e = tt::launch_trace(ta, s);
@@ -179,6 +237,22 @@ tt_status tt_circus_fft_device(const float* d_sino, int n, int rows, double* d_p
         return fail(nullptr, TT_ERR_INVALID, "bad circus_fft arguments");
     cudaError_t e = tt::launch_circus_fft(d_sino, n, rows, d_p, (cudaStream_t)stream);
     return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "circus_fft");
+}
+
+tt_status tt_hermite_device(const float* d_sino, int n, int rows, int orders, double* d_hp, int32_t* d_center,
+                            void* stream) {
+    if (!d_sino || !d_hp || n < 1 || rows < 0 || orders < 1 || orders > tt::max_hermite_orders())
+        return fail(nullptr, TT_ERR_INVALID, "bad hermite arguments");
+    cudaError_t e = tt::launch_hermite(d_sino, n, rows, orders, d_hp, d_center, (cudaStream_t)stream);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "hermite");
+}
+
+int tt_orthonormal_side(int angles) { return tt::orthonormal_side(angles); }
+
+tt_status tt_orthonormal_device(const float* d_img, int h, int w, int angles, float* d_out, void* stream) {
+    if (!d_img || !d_out || h < 1 || w < 1 || angles < 2) return fail(nullptr, TT_ERR_INVALID, "bad orthonormal arguments");
+    cudaError_t e = tt::launch_orthonormal(d_img, h, w, angles, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "orthonormal");
 }
 
 tt_status tt_image_tex_create(const float* d_img, int n, void* stream, tt_image_tex** out) {
@@ -231,6 +305,7 @@ tt_status tt_image_tex_destroy(tt_image_tex* t) {
 }
 
 tt_status tt_trace_device_tex(const tt_trace_desc* d, const tt_image_tex* t, void* stream) {
+    Range r("tt_trace_device_tex");
     tt_status st = check_desc(d);
     if (st != TT_OK) return st;
     if (!t || t->n != d->n) return fail(nullptr, TT_ERR_INVALID, "texture does not match n");
@@ -272,7 +347,6 @@ struct PlanSlot {
     float* img = nullptr;  // linear image(s) (LDG sampler, batched atlas fill)
     float *out = nullptr, *circ = nullptr;
     std::int32_t* med = nullptr;
-    int* unit_done = nullptr;  // fused P stage: per-unit line counters (zeroed once, self-resetting)
     cudaArray_t arr = nullptr;
     cudaTextureObject_t tex = 0;
     std::vector<cudaEvent_t> done;      // per chunk: its rows are final
@@ -280,13 +354,23 @@ struct PlanSlot {
     cudaEvent_t ready = nullptr;        // image uploaded (single-image plans)
     cudaEvent_t free = nullptr;         // the slot's last download finished: buffers reusable
     bool used = false;
+    int* epi[2] = {nullptr, nullptr};   // fused P stage state per compute stream (zeroed, self-resetting)
+    cudaSurfaceObject_t surf = 0;       // batched texture plans: the atlas as a surface (created once)
+    // graph mode: the slot's submission captured once per set of host buffers and replayed on the
+    // slot's own launch stream (the two slots' graphs overlap like the enqueued submissions do)
+    cudaStream_t gs = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t join = nullptr;         // capture: the copy stream joins back into the origin
+    std::array<const void*, 4> key{};   // host buffers the captured graph reads / writes
+    std::uint64_t g_h2d = 0, g_d2h = 0, g_launches = 0;
 };
 
 struct tt_plan {
     tt_ctx* ctx = nullptr;
     tt_plan_desc d{};
     int F = 1, units = 0, pair = 0, chunks = 1, cols = 1, next = 0;
-    bool fused_circus = true;  // P stage as the trace kernel's epilogue (TT_FUSED_CIRCUS=0: separate launch)
+    bool fused_circus = true;
+    int captures = 0;          // graph mode: submissions captured (the rest replayed)  // P stage as the trace kernel's epilogue (TT_FUSED_CIRCUS=0: separate launch)
     float *ctab = nullptr, *stab = nullptr, *wtab = nullptr, *wsoa = nullptr;
     std::vector<PlanSlot> slot;
     cudaStream_t sc[2] = {nullptr, nullptr}, sx = nullptr, si = nullptr;
@@ -303,11 +387,19 @@ void plan_release(tt_plan* p) {
         for (auto* evs : {&sl.done, &sl.uploaded})
             for (cudaEvent_t e : *evs)
                 if (e) cudaEventDestroy(e);
-        for (cudaEvent_t e : {sl.ready, sl.free})
+        for (cudaEvent_t e : {sl.ready, sl.free, sl.join})
             if (e) cudaEventDestroy(e);
+        if (sl.exec) cudaGraphExecDestroy(sl.exec);
+        if (sl.surf) cudaDestroySurfaceObject(sl.surf);
+        if (sl.gs) {
+            cudaStreamSynchronize(sl.gs);
+            cudaStreamDestroy(sl.gs);
+        }
+        for (int* b : sl.epi)
+            if (b) cudaFree(b);
         if (sl.tex) cudaDestroyTextureObject(sl.tex);
         if (sl.arr) cudaFreeArray(sl.arr);
-        for (void* b : {(void*)sl.img, (void*)sl.out, (void*)sl.circ, (void*)sl.med, (void*)sl.unit_done})
+        for (void* b : {(void*)sl.img, (void*)sl.out, (void*)sl.circ, (void*)sl.med})
             if (b) cudaFree(b);
     }
     for (void* b : {(void*)p->ctab, (void*)p->stab, (void*)p->wtab, (void*)p->wsoa})
@@ -371,25 +463,38 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
     }
     for (cudaStream_t* s : {&p->sc[0], &p->sc[1], &p->sx, &p->si})
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+    tt::TraceArgs big;  // the fused P stage's state, sized for the largest launch: all units of all images
+    big.batch = B;
+    big.a_count = p->units;
+    big.pair_stride = p->pair;
+    const std::size_t epi_bytes = tt::epi_state_ints(big) * sizeof(int);
     for (PlanSlot& sl : p->slot) {
         alloc(&sl.img, B * N2 * 4);
         alloc(&sl.out, rows * p->F * n * 4);
         if (d->full) alloc(&sl.med, rows * 2 * n * 4);
-        if (d->features) {
-            alloc(&sl.circ, rows * tt::kNumF * 3 * 4);
-            alloc(&sl.unit_done, std::size_t(B) * p->units * 4);
-            if (e == cudaSuccess) e = cudaMemsetAsync(sl.unit_done, 0, std::size_t(B) * p->units * 4, p->sc[0]);
-        }
+        if (d->features) alloc(&sl.circ, rows * tt::kNumF * 3 * 4);
         sl.done.resize(p->chunks, nullptr);
         sl.uploaded.resize(p->chunks, nullptr);
         for (auto* evs : {&sl.done, &sl.uploaded})
             for (auto& ev : *evs)
                 if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-        for (cudaEvent_t* ev : {&sl.ready, &sl.free})
+        for (cudaEvent_t* ev : {&sl.ready, &sl.free, &sl.join})
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
         if (e == cudaSuccess && ctx->sampler == int(tt::Sampler::Texture))
             e = B > 1 ? tt::make_image_atlas(sl.img, n, B, (long long)N2, p->sc[0], &sl.arr, &sl.tex, &p->cols)
                       : tt::make_image_texture(sl.img, n, p->sc[0], &sl.arr, &sl.tex);
+        if (e == cudaSuccess && B > 1 && sl.arr) {
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypeArray;
+            rd.res.array.array = sl.arr;
+            e = cudaCreateSurfaceObject(&sl.surf, &rd);
+        }
+        if (e == cudaSuccess && d->graph) e = cudaStreamCreateWithFlags(&sl.gs, cudaStreamNonBlocking);
+        if (d->features)
+            for (int k = 0; k < 2; ++k) {
+                alloc(&sl.epi[k], epi_bytes);
+                if (e == cudaSuccess) e = cudaMemsetAsync(sl.epi[k], 0, epi_bytes, p->sc[0]);
+            }
     }
     if (e != cudaSuccess) {
         plan_release(p);
@@ -404,6 +509,22 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
         e = cudaMemcpyAsync(p->wtab, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, p->sc[0]);
         if (e == cudaSuccess) e = tt::launch_weights_soa(p->wtab, n, p->wsoa, p->sc[0]);
     }
+    if (e == cudaSuccess) {  // set the kernels' launch attributes now (not inside a graph capture later)
+        tt::TraceArgs ta;
+        ta.n = n;
+        ta.a_count = 0;
+        ta.full = d->full != 0;
+        ta.wsoa = p->wsoa;
+        ta.batch = B;
+        ta.img0 = B > 1 ? 1 : 0;
+        ta.sampler = ctx->sampler == int(tt::Sampler::Texture) ? tt::Sampler::Texture : tt::Sampler::Global;
+        e = tt::launch_trace(ta, p->sc[0]);
+        if (e == cudaSuccess && B > 1) {  // a one-image chunk at the atlas origin uses the plain-texture kernel
+            ta.batch = 1;
+            ta.img0 = 0;
+            e = tt::launch_trace(ta, p->sc[0]);
+        }
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->sc[0]);
     if (e != cudaSuccess) {
         plan_release(p);
@@ -414,6 +535,7 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
 }
 
 tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int32_t* h_med, float* h_circ) {
+    Range r("tt_plan_submit");
     if (!p || !h_img) return fail(p ? p->ctx : nullptr, TT_ERR_INVALID, "bad plan run arguments");
     tt_ctx* ctx = p->ctx;
     if (ctx->destroyed) return fail(ctx, TT_ERR_INVALID, "context destroyed");
@@ -433,9 +555,30 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
     const bool tex = ctx->sampler == int(tt::Sampler::Texture);
     // the slot's previous submission must have fully drained (its kernels read the texture,
     // its downloads read the outputs) before this one overwrites them
-    if (sl.used) ok(cudaStreamWaitEvent(p->si, sl.free, 0));
+    const bool graph = d.graph != 0;
+    if (sl.used) ok(cudaStreamWaitEvent(graph ? sl.gs : p->si, sl.free, 0));
     sl.used = true;
-    auto trace_args = [&](int u0, int u1, int b0, int b1) {
+    // Graph mode (tt_plan_desc.graph): the whole submission below -- upload, chunked launches on two
+    // streams, downloads, P stage -- is captured into one CUDA graph per slot and host-buffer set,
+    // then replayed with a single cudaGraphLaunch (one host call instead of ~4 + 3 per chunk).
+    const std::array<const void*, 4> key{h_img, h_out, h_med, h_circ};
+    if (graph && sl.exec && sl.key == key) {
+        ok(cudaGraphLaunch(sl.exec, sl.gs));
+        ok(cudaEventRecord(sl.free, sl.gs));
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "plan graph launch");
+        ctx->c.bytes_h2d += sl.g_h2d;
+        ctx->c.bytes_d2h += sl.g_d2h;
+        ctx->c.gpu_kernel_launches += sl.g_launches;
+        return TT_OK;
+    }
+    if (graph) {
+        if (sl.exec) {
+            cudaGraphExecDestroy(sl.exec);
+            sl.exec = nullptr;
+        }
+        ok(cudaStreamBeginCapture(p->si, cudaStreamCaptureModeThreadLocal));
+    }
+    auto trace_args = [&](int u0, int u1, int b0, int b1, int stream_k) {
         tt::TraceArgs ta;
         ta.img = sl.img;
         ta.tex = sl.tex;
@@ -456,9 +599,9 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
         ta.full = d.full != 0;
         ta.batch = b1 - b0;
         ta.img0 = b0;
-        if (d.features && p->fused_circus) {  // fused P stage: the rows' circus features, per-unit counters
+        if (d.features && p->fused_circus) {  // fused P stage: the rows' circus features
             ta.circ = sl.circ + rows0 * row_c;
-            ta.unit_done = sl.unit_done + std::size_t(b0) * p->units + u0;
+            ta.epi = sl.epi[stream_k];  // one state block per slot and compute stream (its launches are ordered)
         }
         return ta;
     };
@@ -488,7 +631,7 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
         for (int c = 0; c < p->chunks && e == cudaSuccess; ++c) {
             const int u0 = int((long long)p->units * c / p->chunks), u1 = int((long long)p->units * (c + 1) / p->chunks);
             cudaStream_t s = p->sc[c & 1];
-            tt::TraceArgs ta = trace_args(u0, u1, 0, 1);
+            tt::TraceArgs ta = trace_args(u0, u1, 0, 1, c & 1);
             if (!ok(tt::launch_trace(ta, s))) break;
             launches += tt::trace_launch_count(ta);
             ok(cudaEventRecord(sl.done[c], s));
@@ -520,10 +663,10 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
             cudaStream_t s = p->sc[0];
             ok(cudaStreamWaitEvent(s, sl.uploaded[c], 0));
             if (tex) {
-                ok(tt::fill_image_atlas(sl.arr, sl.img + b0 * N2, n, int(cnt), (long long)N2, p->cols, s, b0));
+                ok(tt::fill_image_atlas_surf(sl.surf, sl.img + b0 * N2, n, int(cnt), (long long)N2, p->cols, s, b0));
                 ++launches;
             }
-            tt::TraceArgs ta = trace_args(0, p->units, b0, b1);
+            tt::TraceArgs ta = trace_args(0, p->units, b0, b1, 0);
             if (!ok(tt::launch_trace(ta, s))) break;
             launches += tt::trace_launch_count(ta);
             const std::size_t r0 = std::size_t(b0) * units_all, rows = cnt * units_all;
@@ -541,7 +684,26 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
             }
         }
     }
-    ok(cudaEventRecord(sl.free, p->sx));  // every download (and, before them, every kernel) of the slot
+    if (graph) {
+        ok(cudaEventRecord(sl.join, p->sx));  // the copy stream (which waited on every chunk) joins the origin
+        ok(cudaStreamWaitEvent(p->si, sl.join, 0));
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(p->si, &g);  // always ends the capture
+        ok(ce);
+        if (e == cudaSuccess) ok(cudaGraphInstantiate(&sl.exec, g, 0));
+        if (g) cudaGraphDestroy(g);
+        if (e == cudaSuccess) {
+            ++p->captures;
+            sl.key = key;
+            sl.g_h2d = h2d;
+            sl.g_d2h = d2h;
+            sl.g_launches = launches;
+            ok(cudaGraphLaunch(sl.exec, sl.gs));
+            ok(cudaEventRecord(sl.free, sl.gs));
+        }
+    } else {
+        ok(cudaEventRecord(sl.free, p->sx));  // every download (and, before them, every kernel) of the slot
+    }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "plan submit");
     ctx->c.bytes_h2d += h2d;
     ctx->c.bytes_d2h += d2h;
@@ -550,6 +712,7 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
 }
 
 tt_status tt_plan_wait(tt_plan* p) {
+    Range r("tt_plan_wait");
     if (!p) return fail(nullptr, TT_ERR_INVALID, "null plan");
     DeviceGuard guard(p->ctx->device);
     cudaError_t e = cudaSuccess;
@@ -557,6 +720,11 @@ tt_status tt_plan_wait(tt_plan* p) {
         const cudaError_t x = cudaStreamSynchronize(s);
         if (e == cudaSuccess) e = x;
     }
+    for (const PlanSlot& sl : p->slot)
+        if (sl.gs) {
+            const cudaError_t x = cudaStreamSynchronize(sl.gs);
+            if (e == cudaSuccess) e = x;
+        }
     return e == cudaSuccess ? TT_OK : cuda_fail(p->ctx, e, "plan wait");
 }
 
@@ -569,6 +737,12 @@ tt_status tt_plan_run(tt_plan* p, const float* h_img, float* h_out, std::int32_t
 tt_status tt_plan_chunks(const tt_plan* p, int* chunks) {
     if (!p || !chunks) return fail(nullptr, TT_ERR_INVALID, "null argument");
     *chunks = p->chunks;
+    return TT_OK;
+}
+
+tt_status tt_plan_captures(const tt_plan* p, int* captures) {
+    if (!p || !captures) return fail(nullptr, TT_ERR_INVALID, "null argument");
+    *captures = p->captures;
     return TT_OK;
 }
 

@@ -44,8 +44,11 @@ struct TraceArgs {
     long long img_stride = 0;     // elements between images (0: n*n) -- Global sampler
     int atlas_cols = 1;           // texture atlas tiles per row -- Texture sampler
     float* circ = nullptr;        // full: fused P stage -- [rows][6][3] circus features of the launch's rows
-    int* unit_done = nullptr;     // with circ: [batch * a_count] zeroed line counters (left zeroed)
+    int* epi = nullptr;           // with circ: epi_state_ints() zeroed ints (left zeroed); one per concurrent launch
 };
+
+// Size (ints) of the fused P stage's state for a launch (header, unit counters, row queue).
+std::size_t epi_state_ints(const TraceArgs& a);
 
 // Slots (lanes) per line of the fused kernel for side n: 8/16/32 (one warp
 // segment) or 32W (W warps); T0-only launches with n > 1024 use 32 -- the
@@ -110,6 +113,14 @@ cudaError_t launch_circus(const float* sino, int n, int rows, float* circ, cudaS
 // Spectral P-functional sum_k |F(s)_k|^4 of each row, n <= max_circus_fft_n().
 cudaError_t launch_circus_fft(const float* sino, int n, int rows, double* pout, cudaStream_t s);
 int max_circus_fft_n();
+// Hermite P-functionals H_0..H_{orders-1} of each row around its weighted median:
+// hp[row][orders] (f64), center[row] = the median index (may be null); orders <= max_hermite_orders().
+cudaError_t launch_hermite(const float* sino, int n, int rows, int orders, double* hp, int32_t* center, cudaStream_t s);
+int max_hermite_orders();
+// Orthonormal (square) sinogram input: h x w image resampled to s x s, s = orthonormal_side(A) =
+// ceil(A / sqrt 2), centred in an A x A frame.
+int orthonormal_side(int angles);
+cudaError_t launch_orthonormal(const float* img, int h, int w, int angles, float* out, cudaStream_t s);
 
 // Texture atlas of `batch` images (image b at tile (b % cols, b / cols)),
 // 32-bit texels holding the float bits.
@@ -120,6 +131,9 @@ cudaError_t make_image_atlas(const float* imgs, int n, int batch, long long stri
 // imgs (image b0 first; stream-ordered).
 cudaError_t fill_image_atlas(cudaArray_t arr, const float* imgs, int n, int batch, long long stride, int cols,
                              cudaStream_t s, int b0 = 0);
+// The same through an existing surface object of the atlas array (no per-call object: graph-capturable).
+cudaError_t fill_image_atlas_surf(cudaSurfaceObject_t surf, const float* imgs, int n, int batch, long long stride,
+                                  int cols, cudaStream_t s, int b0 = 0);
 
 // 8-bit gray/RGB picture (h x w x ch) -> n x n f32 gray, centred, zero padded.
 cudaError_t launch_prep(const uint8_t* pix, int h, int w, int ch, int n, float* img, cudaStream_t s);

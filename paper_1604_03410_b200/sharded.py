@@ -26,6 +26,12 @@ after that broadcast, so no rank overwrites rows that are still being read.
 every GPU): the device-resident leg of bench.py.  Results equal one
 single-GPU launch bit-for-bit (tests/test_sharded_gpu.py).
 
+Failure detection: every collective is issued asynchronously and its Work
+kept; ``check()`` (called by ``wait``) raises the first communicator error
+(NCCL async errors surface through torch's watchdog when
+TORCH_NCCL_ASYNC_ERROR_HANDLING is on -- ``init_process_group`` below sets it
+and a bounded timeout).  Each step is bracketed by NVTX ranges.
+
 The reference has no multi-device code; the
 per-rank launch is tt_trace_device_tex (include/tt_b200.h), the drop-in
 kernel entry.
@@ -35,6 +41,24 @@ from __future__ import annotations
 from . import shard
 from .trace import (NF, image_texture, image_texture_destroy, image_texture_update, make_tables, trace_device,
                     weights_soa)
+
+
+def init_process_group(backend: str = "nccl", device: int | None = None, timeout_s: float = 300.0):
+    """torch.distributed.init_process_group for the sharded path: NCCL async-error handling on (a
+    failed or hung peer tears the job down instead of hanging it), a bounded collective timeout, and
+    the rank's device bound for NCCL."""
+    import datetime
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+    kw = {"timeout": datetime.timedelta(seconds=timeout_s)}
+    if backend == "nccl" and device is not None:
+        kw["device_id"] = torch.device("cuda", device)
+    dist.init_process_group(backend, **kw)
+    return dist
 
 
 def chunk_bounds(cnt: int, chunks: int, c: int):
@@ -89,6 +113,7 @@ class ShardedTrace:
         self.peer, self._close = shard.share_device_buffers(ptrs if is_root else [], dist, device, src=root,
                                                             group=group)
         self.step = 0
+        self._works = []
         self.copy_done = [None] * self.nslots
         self.up_done = [None, None]
 
@@ -115,7 +140,9 @@ class ShardedTrace:
         ev.record(self.stream)
         self.sig_stream.wait_event(ev)
         with torch.cuda.stream(self.sig_stream):
-            self.dist.all_reduce(self.signal[c], group=self.group)
+            w = self.dist.all_reduce(self.signal[c], group=self.group, async_op=True)
+            w.wait()  # the signal stream (not the host) waits for the collective
+            self._works.append(w)
 
     def _rows(self, c: int):
         """Row ranges [r0, r1) of chunk c over every shard (forward and mirror halves)."""
@@ -154,7 +181,8 @@ class ShardedTrace:
         """Device-resident step: the shard kernels (image already in every rank's slot 0) with
         their chunk signals, on self.stream (enqueue only)."""
         slot = self.step % self.nslots
-        self._body(slot, 0)
+        with self.torch.cuda.nvtx.range("ShardedTrace.run_device"):
+            self._body(slot, 0)
         self.step += 1
 
     def upload(self, host_img) -> None:
@@ -181,14 +209,34 @@ class ShardedTrace:
                 self.stream.wait_event(self.up_done[k])
             if self.copy_done[slot] is not None:  # the slot's previous downloads are finished
                 self.stream.wait_event(self.copy_done[slot])
-        with torch.cuda.stream(self.stream):
-            self.dist.broadcast(self.img[k], src=self.root, group=self.group)
-        self._body(slot, k, host_out, host_med)
+        with torch.cuda.nvtx.range("ShardedTrace.submit"):
+            with torch.cuda.stream(self.stream):
+                w = self.dist.broadcast(self.img[k], src=self.root, group=self.group, async_op=True)
+                w.wait()
+                self._works.append(w)
+            self._body(slot, k, host_out, host_med)
         self.step += 1
 
     def wait(self) -> None:
         for s in (self.up_stream, self.stream, self.sig_stream, self.copy_stream):
             s.synchronize()
+        self.check()
+
+    def check(self) -> None:
+        """Raise the first error any finished collective of this object reported (communicator
+        aborted, timeout); forget the finished ones."""
+        live = []
+        for w in self._works:
+            if w.is_completed():
+                try:
+                    exc = w.exception()
+                except Exception:  # backends without per-work exceptions (errors then surface from wait())
+                    exc = None
+                if exc is not None:
+                    raise RuntimeError(f"ShardedTrace collective failed: {exc}")
+            else:
+                live.append(w)
+        self._works = live
 
     @property
     def out(self):

@@ -26,6 +26,8 @@ CIRCUS = KernelAst("circus", ["sino", "n", "rows", "circ"])
 CIRCUS_FFT = KernelAst("circus_fft", ["sino", "n", "rows", "pf"])
 TRACE_T05_BATCH = KernelAst("trace_t05_batch", ["img", "n", "ctab", "stab", "wtab", "out", "med", "a0", "batch"])
 RADON = KernelAst("radon", ["img", "n", "ctab", "stab", "out", "a0"])
+HERMITE = KernelAst("hermite", ["sino", "n", "rows", "orders", "hp", "center"])
+ORTHONORMAL = KernelAst("orthonormal", ["img", "h", "w", "angles", "out"])
 
 
 def make_tables(n: int, a_total: int):
@@ -190,17 +192,24 @@ class Plan:
 
     def __init__(self, ctx: DeviceContext, n: int, angles: int, full: bool = True, a0: int = 0,
                  a_count: int | None = None, features: bool = False, batch: int = 1, chunks: int = 0,
-                 slots: int = 0, pair_stride: int = 0):
+                 slots: int = 0, pair_stride: int = 0, graph: bool = False):
         self.ctx, self.n, self.full, self.batch = ctx, n, full, batch
         self.a_count = angles - a0 if a_count is None else a_count
         self.features = features and full
         d = _lib.PlanDesc(n, angles, a0, self.a_count, int(full), int(self.features), batch, chunks, slots,
-                          pair_stride)
+                          pair_stride, int(graph))
         self._p = C.c_void_p()
         _check(lib.tt_plan_create(ctx._p, C.byref(d), C.byref(self._p)), ctx._p)
         c = C.c_int()
         _check(lib.tt_plan_chunks(self._p, C.byref(c)))
         self.chunks = c.value
+
+    @property
+    def captures(self) -> int:
+        """Graph mode: submissions captured into CUDA graphs so far (tt_plan_captures)."""
+        c = C.c_int()
+        _check(lib.tt_plan_captures(self._p, C.byref(c)))
+        return c.value
 
     def run(self, img, out=None, med=None, circ=None) -> None:
         """Synchronous: returns with the host outputs filled."""
@@ -348,6 +357,51 @@ def circus_fft(ctx: DeviceContext, sino: np.ndarray):
     if not rep.ok():
         raise RuntimeError(f"circus_fft launch trapped: {rep.trap}")
     return pf
+
+
+def hermite(ctx: DeviceContext, sino: np.ndarray, orders: int = 4):
+    """Hermite P-functionals H_0..H_{orders-1} of host sinogram rows around each row's weighted median
+     through cuda_launch: returns (hp f64 [..., orders], center i32 [...])."""
+    sino = np.ascontiguousarray(sino, np.float32)
+    n = sino.shape[-1]
+    rows = sino.size // n
+    hp = np.empty(sino.shape[:-1] + (orders,), np.float64)
+    center = np.empty(sino.shape[:-1], np.int32)
+    rep = cuda_launch(ctx, HERMITE, GridConfig(((rows + 7) // 8, 1, 1), (256, 1, 1)),
+                      [cu_in(sino), np.int32(n), np.int32(rows), np.int32(orders), cu_out(hp), cu_out(center)])
+    if not rep.ok():
+        raise RuntimeError(f"hermite launch trapped: {rep.trap}")
+    return hp, center
+
+
+def hermite_device(sino_ptr: int, n: int, rows: int, orders: int, hp_ptr: int, center_ptr: int = 0,
+                   stream: int = 0) -> None:
+    """Hermite P-functionals of `rows` device sinogram rows (tt_hermite_device)."""
+    _check(lib.tt_hermite_device(C.c_void_p(sino_ptr), n, rows, orders, C.c_void_p(hp_ptr),
+                                 C.c_void_p(center_ptr or None), C.c_void_p(stream)))
+
+
+def orthonormal_side(angles: int) -> int:
+    """Side s = ceil(angles / sqrt 2) the image is resampled to for a square sinogram."""
+    return lib.tt_orthonormal_side(angles)
+
+
+def orthonormal_image(ctx: DeviceContext, img: np.ndarray, angles: int) -> np.ndarray:
+    """The orthonormal (square) sinogram input frame of a host image through
+    cuda_launch: img (h x w) resampled to s x s and centred in angles x angles."""
+    img = np.ascontiguousarray(img, np.float32)
+    h, w = img.shape
+    out = np.empty((angles, angles), np.float32)
+    rep = cuda_launch(ctx, ORTHONORMAL, GridConfig((1, 1, 1), (256, 1, 1)),
+                      [cu_in(img), np.int32(h), np.int32(w), np.int32(angles), cu_out(out)])
+    if not rep.ok():
+        raise RuntimeError(f"orthonormal launch trapped: {rep.trap}")
+    return out
+
+
+def orthonormal_device(img_ptr: int, h: int, w: int, angles: int, out_ptr: int, stream: int = 0) -> None:
+    """tt_orthonormal_device: device image -> device angles x angles frame."""
+    _check(lib.tt_orthonormal_device(C.c_void_p(img_ptr), h, w, angles, C.c_void_p(out_ptr), C.c_void_p(stream)))
 
 
 def image_texture(img_ptr: int, n: int, stream: int = 0):

@@ -151,3 +151,41 @@ def test_overlapping_submissions_equal_separate_runs(ctx, slots):
     for (o, m, c), (ro, rm, rc) in zip(outs, refs):
         assert np.array_equal(_bits(o), _bits(ro)) and np.array_equal(m, rm) and np.array_equal(_bits(c), _bits(rc))
     plan.destroy()
+
+
+@pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
+@pytest.mark.parametrize("n,A,batch,chunks", [(256, 360, 1, 0), (256, 40, 1, 3), (128, 12, 3, 2)])
+def test_graph_plan_replays_the_captured_submission(ctx, sampler, n, A, batch, chunks):
+    """tt_plan_desc.graph: the first submission per slot and host-buffer set is captured into a CUDA
+    graph and later ones replay it (the steady state: one input buffer refilled per image, the
+    output buffers alternating with the two slots); outputs (sinograms, medians, fused circus)
+    equal the enqueued plan's bit for bit, new host buffers re-capture, counters advance per
+    submission."""
+    ctx.set_sampler(sampler)
+    imgs = [np.stack([tt.synth_image(kind, n, 3 + k + b) for b in range(batch)]) for k, kind in
+            enumerate((tt.PHANTOM, tt.DISK, tt.SPARSE, tt.PHANTOM))]
+    if batch == 1:
+        imgs = [im[0] for im in imgs]
+    ref_plan = tt.Plan(ctx, n, A, features=True, batch=batch, chunks=chunks)
+    gplan = tt.Plan(ctx, n, A, features=True, batch=batch, chunks=chunks, graph=True, slots=2)
+    shape = ((batch,) if batch > 1 else ()) + (A,)
+    bufs = [(np.zeros(shape + (NF, n), np.float32), np.zeros(shape + (2, n), np.int32),
+             np.zeros(shape + (NF, 3), np.float32)) for _ in range(2)]
+    h_img = np.empty_like(imgs[0])
+    for j in range(8):
+        h_img[...] = imgs[j % len(imgs)]
+        o, m, c = bufs[j % 2]
+        c0 = ctx.counters()
+        gplan.run(h_img, o, m, c)
+        c1 = ctx.counters()
+        ro, rm, rc = (np.empty_like(x) for x in (o, m, c))
+        ref_plan.run(h_img, ro, rm, rc)
+        assert np.array_equal(_bits(o), _bits(ro)) and np.array_equal(m, rm) and np.array_equal(_bits(c), _bits(rc))
+        assert c1["bytes_h2d"] - c0["bytes_h2d"] == h_img.nbytes
+        assert c1["bytes_d2h"] - c0["bytes_d2h"] == o.nbytes + m.nbytes + c.nbytes
+    assert gplan.captures == 2  # one per slot; the other six submissions replayed
+    other = np.empty_like(bufs[0][0])
+    gplan.run(h_img, other)  # a different buffer set re-captures
+    assert gplan.captures == 3 and np.array_equal(_bits(other), _bits(bufs[1][0]))
+    gplan.destroy()
+    ref_plan.destroy()

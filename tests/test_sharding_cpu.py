@@ -81,3 +81,37 @@ def test_two_rank_gloo_orientation_gather_is_bit_exact():
         p.join(timeout=120)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) is True
+
+
+def _init_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["RANK"], os.environ["WORLD_SIZE"] = str(rank), str(world)
+    os.environ.pop("TORCH_NCCL_ASYNC_ERROR_HANDLING", None)
+    from paper_1604_03410_b200.sharded import chunk_bounds, init_process_group
+    d = init_process_group("gloo", timeout_s=60)
+    t = torch.ones(1)
+    w = d.all_reduce(t, async_op=True)
+    w.wait()
+    ok = t.item() == world and os.environ["TORCH_NCCL_ASYNC_ERROR_HANDLING"] == "1"
+    # chunk bounds partition every shard
+    for cnt in (0, 1, 5, 90):
+        for ch in (1, 3, 4):
+            got = [u for c in range(ch) for u in range(*chunk_bounds(cnt, ch, c))]
+            ok &= got == list(range(cnt))
+    q.put(ok)
+    d.destroy_process_group()
+
+
+def test_sharded_init_sets_async_error_handling_and_timeout():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_init_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=5) is True and q.get(timeout=5) is True
