@@ -295,8 +295,9 @@ def run_ours(args, ws, rank, local):
             tex = image_atlas(img.data_ptr(), n, B, 0, sptr) if B > 1 else image_texture(img.data_ptr(), n, sptr)
         if full:
             tt.weights_soa(wtab.data_ptr(), n, wsoa.data_ptr(), sptr)
-        # the P stage runs as the trace kernel's epilogue (TT_FUSED_CIRCUS=0: a separate circus launch)
-        fused = feats_on and os.environ.get("TT_FUSED_CIRCUS", "1") != "0"
+        # the P stage is a separate circus launch (measured faster than the fused form, DESIGN.md 3.2;
+        # TT_FUSED_CIRCUS=1 selects the P stage inside the trace launch)
+        fused = feats_on and os.environ.get("TT_FUSED_CIRCUS", "0") == "1"
         launches_per_step = 1 + (1 if feats_on and not fused else 0) + (1 if tex is not None and B > 1 else 0)
 
         def step():
@@ -305,7 +306,7 @@ def run_ours(args, ws, rank, local):
             tt.trace_device(img.data_ptr(), n, a0, a_cnt, ctab.data_ptr(), stab.data_ptr(), wtab.data_ptr(),
                             out.data_ptr(), med.data_ptr(), full=full, sampler=args.sampler, stream=sptr, tex=tex,
                             pair_stride=pair, batch=B, wsoa_ptr=wsoa.data_ptr() if full else 0,
-                            circ_ptr=circ.data_ptr() if fused else 0)
+                            circ_ptr=circ.data_ptr() if fused else 0, fused_p=fused)
 
         def features():
             if feats_on and not fused:  # P-functional (circus) stage consuming the sinograms
@@ -445,7 +446,7 @@ def run_ours(args, ws, rank, local):
         d2h = (nb_out + (nb_med if full else 0) if want_sino else 0) + (nb_circ if feats_on else 0)
         api = (f"tt.Plan(graph=True).submit/wait -> tt_plan_submit x steps + tt_plan_wait (per step: one "
                f"cudaGraphLaunch replaying the captured submission: pinned H2D, {chunks} chunked fused-kernel "
-               f"launches with overlapped D2H of finished rows" + (" and the fused P stage" if feats_on else "")
+               f"launches with overlapped D2H of finished rows" + (" and the circus launch" if feats_on else "")
                + f"; two buffer slots, consecutive steps overlap; {caps} captures)")
     if dist:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)

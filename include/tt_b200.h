@@ -274,12 +274,16 @@ typedef struct tt_trace_desc {
                             shard writing straight into the full [A][F][n] sinogram passes
                             out + a0 rows and partner_row = A/2 (batch 1). */
     int32_t flags;       /* TT_TRACE_PEER_OUT: out/med are another GPU's memory (IPC / NVLink):
-                            each thread fences its stores at system scope before it exits */
-    float* circ;         /* optional (full only): the P stage fused into the launch -- circ[row][6][3]
-                            = tt_circus_device over the launch's sinogram rows, computed by the
-                            group that finishes each unit's last line (bit-identical); NULL: none */
+                            each thread fences its stores at system scope before it exits.
+                            TT_TRACE_FUSED_P (texture sampler): circ is computed inside the trace
+                            launch (appended P-CTAs; measured slower) */
+    float* circ;         /* optional (full only): circ[row][6][3] = tt_circus_device over the launch's
+                            sinogram rows (bit-identical): a separate circus launch after the trace
+                            kernel on the same stream, or with TT_TRACE_FUSED_P the P stage fused
+                            into the trace launch; NULL: none */
 } tt_trace_desc;
 #define TT_TRACE_PEER_OUT 1
+#define TT_TRACE_FUSED_P 2
 tt_status tt_trace_device(const tt_trace_desc* d, void* stream);
 
 /* Regroup a [n][8] weight table (tt_make_tables) on device into the fused

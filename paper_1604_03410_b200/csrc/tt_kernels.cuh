@@ -43,11 +43,13 @@ struct TraceArgs {
     int img0 = 0;                 // atlas/array index of the launch's first image (outputs stay launch-relative)
     long long img_stride = 0;     // elements between images (0: n*n) -- Global sampler
     int atlas_cols = 1;           // texture atlas tiles per row -- Texture sampler
-    float* circ = nullptr;        // full: fused P stage -- [rows][6][3] circus features of the launch's rows
+    float* circ = nullptr;        // full: [rows][6][3] circus features of the launch's rows (separate circus launch)
+    bool fuse_circus = false;     // with circ and the texture sampler: the P stage inside the trace launch
     int* epi = nullptr;           // with circ: epi_state_ints() zeroed ints (left zeroed); one per concurrent launch
 };
 
-// Size (ints) of the fused P stage's state for a launch (header, unit counters, row queue).
+// Size (ints) of the fused P stage's state for a launch: per unit a line counter and a finished-row
+// counter (zeroed once; every launch leaves them zeroed).
 std::size_t epi_state_ints(const TraceArgs& a);
 
 // Slots (lanes) per line of the fused kernel for side n: 8/16/32 (one warp

@@ -256,13 +256,13 @@ class Plan:
 def trace_device(img_ptr: int, n: int, a0: int, a_count: int, ctab_ptr: int, stab_ptr: int, wtab_ptr: int,
                  out_ptr: int, med_ptr: int = 0, full: bool = True, sampler: int = 0, stream: int = 0,
                  tex=None, pair_stride: int = 0, batch: int = 1, img_stride: int = 0, wsoa_ptr: int = 0,
-                 partner_row: int = 0, peer_out: bool = False, circ_ptr: int = 0) -> None:
+                 partner_row: int = 0, peer_out: bool = False, circ_ptr: int = 0, fused_p: bool = False) -> None:
     """Raw device-pointer launch (tt_trace_device / tt_trace_device_tex); pair_stride, batch, wsoa as in
-    tt_b200.h (wsoa_ptr: a prepared weights_soa() buffer; 0 converts wtab per call; circ_ptr: the fused
-    P stage's [rows][6][3] output, 0 = none)."""
+    tt_b200.h (wsoa_ptr: a prepared weights_soa() buffer; 0 converts wtab per call; circ_ptr: the
+    [rows][6][3] circus output, 0 = none; fused_p: compute it inside the trace launch, TT_TRACE_FUSED_P)."""
     d = _lib.TraceDesc(img_ptr, n, a0, a_count, int(full), ctab_ptr, stab_ptr, wtab_ptr or None, out_ptr,
                        med_ptr or None, sampler, pair_stride, batch, 0, img_stride, wsoa_ptr or None, partner_row,
-                       1 if peer_out else 0, circ_ptr or None)
+                       (1 if peer_out else 0) | (2 if fused_p else 0), circ_ptr or None)
     if tex is not None:
         _check(lib.tt_trace_device_tex(C.byref(d), tex, C.c_void_p(stream)))
     else:

@@ -27,7 +27,9 @@ sp = stream.cuda_stream
 tt.weights_soa(wt.data_ptr(), n, wsoa.data_ptr(), sp)
 sampler = int(os.environ.get("TT_SAMPLER_ID", "1"))  # 1 texture gather, 0 LDG
 tex = image_texture(img.data_ptr(), n, sp) if sampler == 1 else None
-circ = torch.empty((A, F, 3), device="cuda") if os.environ.get("TT_CIRC") == "1" and full else None  # fused P stage
+# TT_CIRC=1: circus output with the P stage fused into the trace launch; 2: separate circus launch
+circ_mode = os.environ.get("TT_CIRC", "0")
+circ = torch.empty((A, F, 3), device="cuda") if circ_mode in ("1", "2") and full else None
 ts = []
 for i in range(reps + 3):
     with torch.cuda.stream(stream):
@@ -36,7 +38,8 @@ for i in range(reps + 3):
     e0.record(stream)
     tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
                     med.data_ptr() if full else 0, full=full, sampler=sampler, stream=sp, tex=tex,
-                    wsoa_ptr=wsoa.data_ptr(), circ_ptr=circ.data_ptr() if circ is not None else 0)
+                    wsoa_ptr=wsoa.data_ptr(), circ_ptr=circ.data_ptr() if circ is not None else 0,
+                    fused_p=circ_mode == "1")
     e1.record(stream)
     e1.synchronize()
     if i >= 3:

@@ -70,13 +70,15 @@ def test_resident_flow_with_features(ctx):
     assert np.array_equal(circ.view(np.uint32), rc.view(np.uint32))
 
 
+@pytest.mark.parametrize("fused", [0, 1], ids=["separate", "fused"])
 @pytest.mark.parametrize("sampler", [0, 1], ids=["ldg", "tex"])
 @pytest.mark.parametrize("n,A,batch,pair", [(64, 10, 1, 0), (128, 9, 1, 0), (256, 12, 3, 0), (1024, 8, 1, 0),
                                             (1000, 6, 1, 0), (2048, 4, 1, 0), (4096, 2, 1, 0), (256, 16, 1, 8),
                                             (256, 16, 1, 4)])
-def test_fused_circus_epilogue_equals_separate_stage(gpu, n, A, batch, pair, sampler):
-    """tt_trace_desc.circ: the P stage as the trace kernel's epilogue (the group finishing a unit's
-    last line computes its rows) -- bit-identical to tt_circus_device over the same rows, and to the
+def test_trace_circus_output_equals_separate_stage(gpu, n, A, batch, pair, sampler, fused):
+    """tt_trace_desc.circ: the P stage of a raw trace launch -- a separate circus launch on the same
+    stream, or with TT_TRACE_FUSED_P (texture sampler) P-CTAs appended to the trace launch (warp per row,
+    waiting on per-unit line counters) -- bit-identical to tt_circus_device over the same rows, and to the
     oracle's replay; covers sub-warp segments, W > 1 warps per line, batches, unpaired units and
     explicit mirror-half shards."""
     import torch
@@ -94,7 +96,7 @@ def test_fused_circus_epilogue_equals_separate_stage(gpu, n, A, batch, pair, sam
     for _ in range(2):  # the per-unit counters reset themselves: a second launch must work the same
         tt.trace_device(img.data_ptr(), n, 0, a_count, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
                         med.data_ptr(), sampler=sampler, tex=tex, batch=batch, pair_stride=pair,
-                        circ_ptr=circ.data_ptr())
+                        circ_ptr=circ.data_ptr(), fused_p=bool(fused))
     ref = torch.empty_like(circ)
     tt.circus_device(out.data_ptr(), n, batch * a_count * 6, ref.data_ptr())
     torch.cuda.synchronize()
