@@ -391,6 +391,7 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     ta.full = full;
     ta.batch = batch;
     ta.sampler = tt::Sampler(ctx.sampler);
+    if (ta.sampler == tt::Sampler::Tma && !tt::tma_radon_ok(ta)) ta.sampler = tt::Sampler::Texture;
     if (ta.sampler == tt::Sampler::Texture) {
         TexEntry& te = ctx.tex_cache[img.base];
         if (te.arr == nullptr || te.n != n || te.batch != batch) {
@@ -670,10 +671,13 @@ tt_status tt_ctx_create(int device, const tt_caps* caps, tt_ctx** out) {
         std::uint64_t thresh = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
     }
-    // Texture gather is the default sampler (measured faster, profiles/); TT_SAMPLER=ldg selects L1 loads.
-    ctx->sampler = 1;
+    // Default sampler 2: TMA-staged tiles for the T0 (Radon) launches they serve, the texture gather for
+    // everything else -- the faster of the two for each (measured, profiles/r02_tma_radon.txt);
+    // TT_SAMPLER=ldg selects L1 loads, TT_SAMPLER=tex the texture gather for every launch.
+    ctx->sampler = 2;
     const char* smp = std::getenv("TT_SAMPLER");
     if (smp && (std::strcmp(smp, "ldg") == 0 || std::strcmp(smp, "0") == 0)) ctx->sampler = 0;
+    if (smp && (std::strcmp(smp, "tex") == 0 || std::strcmp(smp, "1") == 0)) ctx->sampler = 1;
     ctx->id = ++g_next_ctx_id;
     *out = ctx.release();
     return TT_OK;
@@ -721,7 +725,8 @@ tt_status tt_ctx_device(const tt_ctx* ctx, int* out) {
 
 tt_status tt_ctx_set_sampler(tt_ctx* ctx, int sampler) {
     TT_CHECK_CTX(ctx);
-    if (sampler != 0 && sampler != 1) return fail(ctx, TT_ERR_INVALID, "sampler must be 0 (global) or 1 (texture)");
+    if (sampler < 0 || sampler > 2)
+        return fail(ctx, TT_ERR_INVALID, "sampler must be 0 (global), 1 (texture) or 2 (TMA tiles, T0)");
     ctx->sampler = sampler;
     return TT_OK;
 }

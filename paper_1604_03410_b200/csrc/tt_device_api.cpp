@@ -206,7 +206,14 @@ tt_status tt_trace_device(const tt_trace_desc* d, void* stream) {
     if (cudaError_t e = ws.prepare(ta, s); e != cudaSuccess) return cuda_fail(nullptr, e, "weight table");
     CounterScratch cs;
     if (cudaError_t e = cs.prepare(ta, s); e != cudaSuccess) return cuda_fail(nullptr, e, "circus counters");
-    if (d->sampler == 1) {
+    if (d->sampler == 2) {  // TMA-staged tiles straight from img (T0); other launches: the texture copy below
+        ta.sampler = tt::Sampler::Tma;
+        if (tt::tma_radon_ok(ta)) {
+            cudaError_t e = tt::launch_trace(ta, s);
+            return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "trace kernel");
+        }
+    }
+    if (d->sampler == 1 || d->sampler == 2) {
         reclaim_textures(false);  // copies of earlier calls whose launches have completed
         DeferredTex t;
         cudaGetDevice(&t.device);
@@ -500,7 +507,7 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
                 if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         for (cudaEvent_t* ev : {&sl.ready, &sl.free, &sl.join})
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
-        if (e == cudaSuccess && ctx->sampler == int(tt::Sampler::Texture))
+        if (e == cudaSuccess && ctx->sampler != int(tt::Sampler::Global))
             e = B > 1 ? tt::make_image_atlas(sl.img, n, B, (long long)N2, p->sc[0], &sl.arr, &sl.tex, &p->cols)
                       : tt::make_image_texture(sl.img, n, p->sc[0], &sl.arr, &sl.tex);
         if (e == cudaSuccess && B > 1 && sl.arr) {
@@ -537,7 +544,7 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
         ta.wsoa = p->wsoa;
         ta.batch = B;
         ta.img0 = B > 1 ? 1 : 0;
-        ta.sampler = ctx->sampler == int(tt::Sampler::Texture) ? tt::Sampler::Texture : tt::Sampler::Global;
+        ta.sampler = ctx->sampler != int(tt::Sampler::Global) ? tt::Sampler::Texture : tt::Sampler::Global;
         e = tt::launch_trace(ta, p->sc[0]);
         if (e == cudaSuccess && B > 1) {  // a one-image chunk at the atlas origin uses the plain-texture kernel
             ta.batch = 1;
@@ -572,7 +579,7 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
         if (e == cudaSuccess) e = x;
         return e == cudaSuccess;
     };
-    const bool tex = ctx->sampler == int(tt::Sampler::Texture);
+    const bool tex = ctx->sampler != int(tt::Sampler::Global);  // plans sample through their texture
     // the slot's previous submission must have fully drained (its kernels read the texture,
     // its downloads read the outputs) before this one overwrites them
     const bool graph = d.graph != 0;

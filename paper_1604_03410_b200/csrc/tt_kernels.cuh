@@ -20,6 +20,8 @@ constexpr int kNumF = 6;  // T0..T5
 enum class Sampler : int {
     Global = 0,   // 4 x LDG through L1 (row-major image in HBM/L2)
     Texture = 1,  // 1 x TLD4 (tex2Dgather) on a block-linear cudaArray copy
+    Tma = 2,      // T0 only (n > 1024, n % 4 == 0, one image): TMA-staged shared-memory tiles, 4 x LDS;
+                  // other launches fall back to Texture (tex must then be set; tma_radon_ok())
 };
 
 struct TraceArgs {
@@ -48,6 +50,8 @@ struct TraceArgs {
     int* epi = nullptr;           // with circ: epi_state_ints() zeroed ints (left zeroed); one per concurrent launch
 };
 
+// True when launch_trace serves a Sampler::Tma launch with the TMA tile kernel itself.
+bool tma_radon_ok(const TraceArgs& a);
 // Size (ints) of the fused P stage's state for a launch: per unit a line counter and a finished-row
 // counter (zeroed once; every launch leaves them zeroed).
 std::size_t epi_state_ints(const TraceArgs& a);
