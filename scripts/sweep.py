@@ -4,7 +4,7 @@ CUDA events on the launch stream, L2 flushed before every timed launch.
 Prints one JSON line per point (ms, sinogram samples/s, taps/s, FLOP
 fraction of the measured FFMA peak, fraction of the measured TLD4 gather peak).
 
-  python scripts/sweep.py [--quick] > profiles/sweep_rNN.jsonl
+  python scripts/sweep.py [--quick] [--sampler auto|tex|tma] > profiles/sweep_rNN.jsonl
 """
 import argparse
 import json
@@ -20,7 +20,7 @@ from paper_1604_03410_b200._lib import lib  # noqa: E402
 from paper_1604_03410_b200.trace import image_texture, image_texture_destroy  # noqa: E402
 
 
-def run_point(n, A, full, stream, flush, reps, peak, tpeak):
+def run_point(n, A, full, stream, flush, reps, peak, tpeak, sampler=1):
     F = 6 if full else 1
     c, s, w = tt.make_tables(n, A)
     img = torch.from_numpy(tt.synth_image(tt.DISK, n)).cuda()
@@ -28,13 +28,13 @@ def run_point(n, A, full, stream, flush, reps, peak, tpeak):
     out = torch.empty((A, F, n), device="cuda")
     med = torch.empty((A, 2, n), dtype=torch.int32, device="cuda") if full else None
     sp = stream.cuda_stream
-    tex = image_texture(img.data_ptr(), n, sp)
+    tex = image_texture(img.data_ptr(), n, sp) if sampler == 1 else None
     wsoa = torch.empty(6 * n, device="cuda")
     tt.weights_soa(wt.data_ptr(), n, wsoa.data_ptr(), sp)
 
     def launch():
         tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
-                        med.data_ptr() if full else 0, full=full, sampler=1, stream=sp, tex=tex,
+                        med.data_ptr() if full else 0, full=full, sampler=sampler, stream=sp, tex=tex,
                         wsoa_ptr=wsoa.data_ptr())
 
     for _ in range(2):
@@ -49,20 +49,25 @@ def run_point(n, A, full, stream, flush, reps, peak, tpeak):
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-    image_texture_destroy(tex)
+    if tex is not None:
+        image_texture_destroy(tex)
     ms = sorted(times)[len(times) // 2]
     taps = lib.tt_count_inbounds_taps(n, 0, A, c.ctypes.data, s.ctypes.data)
     flops = bench.FLOPS_PER_TAP[full] * taps
     return {"n": n, "angles": A, "functionals": "T0-T5" if full else "T0", "ms": ms,
+            "sampler": "tma" if sampler == 2 else "tex",
             "samples_per_s": F * A * n / (ms / 1e3), "taps_per_s": taps / (ms / 1e3),
             "tflops": flops / (ms / 1e3) / 1e12, "fp32_frac": flops / (ms / 1e3) / 1e12 / peak,
-            # one TLD4 per sampled tap; mirrored angle pairs share a pass (A/2 passes of n^2 taps)
+            # one TLD4 per sampled tap; mirrored angle pairs share a pass (A/2 passes of n^2 taps); for the
+            # TMA tile kernel (no TLD4) this is the rate relative to the texture-gather ceiling (> 1: beyond it)
             "tex_gather_frac": (A // 2) * n * n / (ms / 1e3) / tpeak}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--sampler", default="auto", choices=["auto", "tex", "tma"],
+                    help="auto (the product default): TMA tiles for the T0 launches they serve, texture otherwise")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     flush = torch.empty(int(256 << 20) // 4, device="cuda")
@@ -78,7 +83,9 @@ def main():
                 if full and n > tt.max_full_n():
                     continue
                 reps = 5 if n * n * A > 4e10 else 10
-                pt = run_point(n, A, full, stream, flush, reps, peak, tpeak)
+                tma_ok = not full and n > 1024 and n % 4 == 0
+                smp = 2 if (args.sampler == "tma" or (args.sampler == "auto" and tma_ok)) else 1
+                pt = run_point(n, A, full, stream, flush, reps, peak, tpeak, smp)
                 pt["fp32_peak_tflops"] = peak
                 pt["tex_peak_gathers_per_s"] = tpeak
                 print(json.dumps(pt), flush=True)
