@@ -302,7 +302,8 @@ tt_status tt_weights_soa(const float* d_wtab, int n, float* d_wsoa, void* stream
  * GPUs of one node, or between processes on one GPU).  The multi-GPU driver
  * hands rank 0's sinogram buffers to every rank, whose fused kernel then
  * writes its orientation shard's rows straight into them (the gather is the
- * kernel's own stores).  Export works for any pointer inside
+ * kernel's own stores; the multi-GPU driver exports
+ * tt_ipc_alloc buffers).  Export works for any pointer inside
  * a cudaMalloc allocation (the handle carries the offset). */
 typedef struct tt_ipc_handle {
     uint8_t bytes[64];
@@ -311,6 +312,12 @@ typedef struct tt_ipc_handle {
 tt_status tt_ipc_export(const void* d_ptr, tt_ipc_handle* out);
 tt_status tt_ipc_import(const tt_ipc_handle* h, int device, void** d_ptr);
 tt_status tt_ipc_close(void* d_ptr);
+/* A dedicated device allocation for exporting (one cudaMalloc per buffer on
+ * `device`): its IPC handle does not depend on any caching allocator's block
+ * layout (e.g. PyTorch's expandable segments).  Freed by tt_ipc_free after
+ * every importer has closed it. */
+tt_status tt_ipc_alloc(int device, size_t bytes, void** d_ptr);
+tt_status tt_ipc_free(void* d_ptr);
 
 /* P-functionals (circus features) of `rows` sinogram rows of
  * length n on device: circ[row][3] = (total variation, value at the weighted

@@ -114,6 +114,8 @@ _sigs = {
     "tt_ipc_export": (_S, [C.c_void_p, C.POINTER(IpcHandle)]),
     "tt_ipc_import": (_S, [C.POINTER(IpcHandle), C.c_int, C.POINTER(C.c_void_p)]),
     "tt_ipc_close": (_S, [C.c_void_p]),
+    "tt_ipc_alloc": (_S, [C.c_int, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "tt_ipc_free": (_S, [C.c_void_p]),
     "tt_circus_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_circus_fft_device": (_S, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "tt_image_tex_create": (_S, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),

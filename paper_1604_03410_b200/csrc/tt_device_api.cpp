@@ -814,6 +814,21 @@ tt_status tt_ipc_export(const void* d_ptr, tt_ipc_handle* out) {
     return TT_OK;
 }
 
+tt_status tt_ipc_alloc(int device, size_t bytes, void** d_ptr) {
+    if (!d_ptr || bytes == 0) return fail(nullptr, TT_ERR_INVALID, "bad IPC allocation arguments");
+    DeviceGuard guard(device);
+    cudaError_t e = cudaMalloc(d_ptr, bytes);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMalloc (IPC buffer)");
+    e = cudaMemset(*d_ptr, 0, bytes);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "cudaMemset (IPC buffer)");
+}
+
+tt_status tt_ipc_free(void* d_ptr) {
+    if (!d_ptr) return TT_OK;
+    cudaError_t e = cudaFree(d_ptr);
+    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "cudaFree (IPC buffer)");
+}
+
 tt_status tt_ipc_import(const tt_ipc_handle* hd, int device, void** d_ptr) {
     if (!hd || !d_ptr) return fail(nullptr, TT_ERR_INVALID, "null argument");
     DeviceGuard guard(device);

@@ -39,8 +39,8 @@ kernel entry.
 from __future__ import annotations
 
 from . import shard
-from .trace import (NF, image_texture, image_texture_destroy, image_texture_update, make_tables, trace_device,
-                    weights_soa)
+from .trace import (NF, IpcBuffer, image_texture, image_texture_destroy, image_texture_update, make_tables,
+                    trace_device, weights_soa)
 
 
 def init_process_group(backend: str = "nccl", device: int | None = None, timeout_s: float = 300.0):
@@ -99,8 +99,11 @@ class ShardedTrace:
             self.signal = [torch.zeros(1, device=dev) for _ in range(self.chunks)]
             is_root = self.rank == root
             self.slots = slots if is_root else 0
-            self.outs = [torch.empty((angles, self.F, n), device=dev) for _ in range(self.slots)]
-            self.meds = [torch.empty((angles, 2, n), dtype=torch.int32, device=dev) for _ in range(self.slots)]
+            # exported buffers are dedicated allocations (IpcBuffer), not caching-allocator blocks
+            self._ipc_bufs = ([IpcBuffer(device, (angles, self.F, n), "float32") for _ in range(self.slots)],
+                              [IpcBuffer(device, (angles, 2, n), "int32") for _ in range(self.slots)])
+            self.outs = [torch.as_tensor(b, device=dev) for b in self._ipc_bufs[0]]
+            self.meds = [torch.as_tensor(b, device=dev) for b in self._ipc_bufs[1]]
         if full:
             weights_soa(self.wtab.data_ptr(), n, self.wsoa.data_ptr(), self.stream.cuda_stream)
         self.tex = image_texture(self.img[0].data_ptr(), n, self.stream.cuda_stream) if sampler == 1 else None
@@ -250,6 +253,9 @@ class ShardedTrace:
         self.wait()
         self.dist.barrier(group=self.group)  # no rank still writes into rank 0's buffers
         self._close()
+        self.dist.barrier(group=self.group)  # every mapping closed before rank 0 frees the exported buffers
+        self.outs = self.meds = []
+        self._ipc_bufs = ([], [])
         if self.tex is not None:
             image_texture_destroy(self.tex)
             self.tex = None

@@ -318,6 +318,33 @@ def ipc_close(ptr: int) -> None:
     _check(lib.tt_ipc_close(C.c_void_p(ptr)))
 
 
+class IpcBuffer:
+    """A dedicated device allocation made for export (tt_ipc_alloc: one cudaMalloc, zero-filled), so its
+    IPC handle is independent of the caching allocator's block layout.  Exposes
+    ``__cuda_array_interface__`` (``torch.as_tensor(buf, device=...)`` views it without a copy); freed
+    when the object is released (after every importer has closed its mapping)."""
+
+    def __init__(self, device: int, shape, dtype):
+        import numpy as np
+        self.shape = tuple(int(x) for x in shape)
+        self.dtype = np.dtype(dtype)
+        nbytes = int(np.prod(self.shape)) * self.dtype.itemsize
+        p = C.c_void_p()
+        _check(lib.tt_ipc_alloc(int(device), max(nbytes, 1), C.byref(p)))
+        self.ptr = p.value
+        self.device = device
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": self.shape, "typestr": self.dtype.str, "data": (self.ptr, False), "version": 3,
+                "strides": None}
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib.tt_ipc_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
 def weights_soa(wtab_ptr: int, n: int, wsoa_ptr: int, stream: int = 0) -> None:
     """Regroup a device [n][8] weight table into the pass-2 layout (tt_weights_soa; 24n bytes)."""
     _check(lib.tt_weights_soa(C.c_void_p(wtab_ptr), n, C.c_void_p(wsoa_ptr), C.c_void_p(stream)))

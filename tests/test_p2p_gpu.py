@@ -68,3 +68,22 @@ def test_direct_write_shards_assemble_the_full_sinogram(gpu, world, n, A):
         p.join(timeout=240)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=10) is True
+
+
+def test_ipc_buffer_is_a_dedicated_exportable_allocation(gpu):
+    """tt_ipc_alloc buffers (what ShardedTrace exports): zero-filled, viewed by torch without a copy, and
+    exported at offset 0 of their own allocation (independent of the caching allocator's blocks)."""
+    import torch
+
+    from paper_1604_03410_b200.trace import IpcBuffer, ipc_export
+
+    buf = IpcBuffer(gpu, (3, 5, 7), "float32")
+    t = torch.as_tensor(buf, device=f"cuda:{gpu}")
+    assert t.shape == (3, 5, 7) and t.data_ptr() == buf.ptr and float(t.abs().sum()) == 0.0
+    t.fill_(2.5)
+    assert float(torch.as_tensor(buf, device=f"cuda:{gpu}").sum()) == 2.5 * 105
+    h = ipc_export(buf.ptr + 4 * 35)  # a pointer inside it: the handle carries the offset
+    assert int.from_bytes(h[64:72], "little") == 4 * 35
+    del t
+    del buf
+    torch.cuda.synchronize()

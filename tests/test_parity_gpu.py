@@ -68,6 +68,31 @@ def test_radon_t0_bit_exact(ctx, n, A, kind, sampler):
     assert fails == 0, st
 
 
+@pytest.mark.parametrize("sampler", [0, 1, 2], ids=["ldg", "tex", "tma"])
+@pytest.mark.parametrize("n,A,full", [(64, 16, True), (300, 12, True), (1028, 8, False)])
+def test_non_finite_pixels_stay_local(ctx, n, A, full, sampler):
+    """Inf / NaN pixels (one at the corner (0,0), which every out-of-range LDG tap addresses) reach
+    only the lines whose in-range taps touch them: every other line is bit-exact against the replay,
+    and a line is non-finite exactly where the replay's is (out-of-range taps select +0,
+    they never multiply a fetched pixel by 0)."""
+    img = tt.synth_image(tt.PHANTOM, n)
+    img[0, 0] = np.nan
+    img[n // 2, 1] = np.inf
+    img[1, n - 2] = -np.inf
+    tr, out, med = _run(ctx, img, n, A, full=full, sampler=sampler)
+    rout, rmed, _, _ = O.transform(img, n, tr.ctab, tr.stab, tr.wtab, mode=O.REPLAY, full=full)
+    F = 6 if full else 1
+    out, rout = out.reshape(A, F, n), rout.reshape(A, F, n)
+    bad = ~np.isfinite(rout).all(axis=1)  # [A][n] lines with a non-finite functional in the replay
+    assert bad.sum() < bad.size // 4, "most lines non-finite: out-of-range taps leak the bad pixels"
+    assert np.array_equal(~np.isfinite(out).all(axis=1), bad)
+    good = np.broadcast_to(~bad[:, None, :], out.shape)
+    assert _bitwise_equal(out[good], rout[good])
+    if full:
+        mg = np.broadcast_to(~bad[:, None, :], med.shape)
+        assert np.array_equal(med[mg], rmed[mg])
+
+
 def test_radon_equals_t0_of_full_kernel(ctx):
     n, A = 300, 17
     img = tt.synth_image(tt.PHANTOM, n)
