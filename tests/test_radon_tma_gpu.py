@@ -3,7 +3,7 @@
 The tile kernel keeps the texture kernel's per-tap arithmetic, slot order and
 butterfly, so its sinogram must equal the texture path's bit for bit, and the
 oracle's replay of the NS = 32 schedule (TTO_REPLAY); launches it does not
-serve (T0-T5, n <= 1024, n % 4 != 0) fall back to the texture gather.
+serve (T0-T5, n <= 768, n % 4 != 0) fall back to the texture gather.
 """
 import numpy as np
 import pytest
@@ -33,7 +33,8 @@ def _raw(img, n, a0, a_count, A_total, sampler, pair_stride=0, partner_row=0, fu
     return out.cpu().numpy(), c, s, w
 
 
-@pytest.mark.parametrize("n,A,kind", [(1028, 6, tt.DISK), (2048, 8, tt.PHANTOM), (3000, 4, tt.SPARSE),
+@pytest.mark.parametrize("n,A,kind", [(516, 6, tt.PHANTOM), (1000, 8, tt.DISK), (1024, 12, tt.SPARSE),
+                                      (1028, 6, tt.DISK), (2048, 8, tt.PHANTOM), (3000, 4, tt.SPARSE),
                                       (4096, 6, tt.DISK), (4100, 3, tt.PHANTOM), (8192, 2, tt.DISK)])
 def test_tma_radon_equals_texture_and_replay(gpu, n, A, kind):
     img = tt.synth_image(kind, n)
@@ -91,7 +92,7 @@ def test_tma_radon_unmirrored_partner(gpu):
     assert _bitwise_equal(outs[0], rout)
 
 
-@pytest.mark.parametrize("n,full", [(1024, False), (1030, False), (2048, True)])
+@pytest.mark.parametrize("n,full", [(512, False), (768, False), (1030, False), (2048, True)])
 def test_tma_sampler_falls_back_to_texture(gpu, n, full):
     """Launches the tile kernel does not serve run the texture gather (same bits as sampler 1)."""
     A = 4
