@@ -75,7 +75,7 @@ class ShardedTrace:
     Outputs on rank 0: ``out`` [A][F][n] f32 and ``med`` [A][2][n] i32."""
 
     def __init__(self, n: int, angles: int, dist, device: int, full: bool = True, chunks: int = 4,
-                 sampler: int = 1, group=None, root: int = 0, slots: int = 2):
+                 sampler: int | None = None, group=None, root: int = 0, slots: int = 2):
         import torch
 
         self.torch, self.dist, self.group, self.root = torch, dist, group, root
@@ -85,6 +85,10 @@ class ShardedTrace:
         self.chunks = max(1, min(chunks, max(1, min(shard.orientation_shard(angles, self.world, r)[1]
                                                         for r in range(self.world)))))
         self.device = torch.device("cuda", device)
+        if sampler is None:  # the measured-faster sampler: TMA tiles for the T0 launches they serve, else texture
+            from .trace import schedule_slots
+            tma = not full and n > 768 and n % 4 == 0 and schedule_slots(n, False) == 32
+            sampler = 2 if tma else 1
         self.sampler = sampler
         dev = self.device
         self.stream = torch.cuda.Stream(dev)       # texture refresh + shard kernels

@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, A, chunks, result):
+def _worker(rank, world, port, n, A, chunks, result, full=True):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -32,8 +32,8 @@ def _worker(rank, world, port, n, A, chunks, result):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    F = 6
-    st = ShardedTrace(n, A, dist, 0, chunks=chunks)
+    F = 6 if full else 1
+    st = ShardedTrace(n, A, dist, 0, chunks=chunks, full=full)  # T0 at n > 768: the TMA tile kernel
     imgs = [tt.synth_image(kind, n) for kind in (tt.PHANTOM, tt.DISK, tt.SPARSE)]
     root = rank == 0
     ok = True
@@ -46,9 +46,10 @@ def _worker(rank, world, port, n, A, chunks, result):
     if root:
         ctx = tt.create_context(0)
         for i, im in enumerate(imgs):
-            ref, rmed, rep = tt.TraceTransform(ctx, n, A)(im)
-            ok &= rep.ok() and np.array_equal(ho[i].numpy().view(np.uint32), ref.view(np.uint32)) \
-                and np.array_equal(hm[i].numpy(), rmed)
+            ref, rmed, rep = tt.TraceTransform(ctx, n, A, full=full)(im)
+            ok &= rep.ok() and np.array_equal(ho[i].numpy().reshape(-1).view(np.uint32), ref.reshape(-1).view(np.uint32))
+            if full:
+                ok &= np.array_equal(hm[i].numpy(), rmed)
         ctx.destroy()
     # device-resident leg: image already in slot 0 on every rank
     st.img[0].copy_(torch.from_numpy(imgs[1]))
@@ -58,23 +59,25 @@ def _worker(rank, world, port, n, A, chunks, result):
     dist.barrier()
     if root:
         ctx = tt.create_context(0)
-        ref, rmed, _ = tt.TraceTransform(ctx, n, A)(imgs[1])
-        ok &= np.array_equal(st.out.cpu().numpy().view(np.uint32), ref.view(np.uint32)) and \
-            np.array_equal(st.med.cpu().numpy(), rmed)
+        ref, rmed, _ = tt.TraceTransform(ctx, n, A, full=full)(imgs[1])
+        ok &= np.array_equal(st.out.cpu().numpy().reshape(-1).view(np.uint32), ref.reshape(-1).view(np.uint32))
+        if full:
+            ok &= np.array_equal(st.med.cpu().numpy(), rmed)
         ctx.destroy()
         result.put(bool(ok))
     st.close()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,A,chunks", [(2, 256, 40, 3), (4, 512, 24, 2), (3, 128, 18, 4)])
-def test_sharded_trace_equals_one_launch(gpu, world, n, A, chunks):
+@pytest.mark.parametrize("world,n,A,chunks,full", [(2, 256, 40, 3, True), (4, 512, 24, 2, True), (3, 128, 18, 4, True),
+                                                   (2, 1024, 16, 2, False)])
+def test_sharded_trace_equals_one_launch(gpu, world, n, A, chunks, full):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, A, chunks, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, A, chunks, q, full)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
