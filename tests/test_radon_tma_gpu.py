@@ -35,7 +35,7 @@ def _raw(img, n, a0, a_count, A_total, sampler, pair_stride=0, partner_row=0, fu
 
 @pytest.mark.parametrize("n,A,kind", [(516, 6, tt.PHANTOM), (1000, 8, tt.DISK), (1024, 12, tt.SPARSE),
                                       (1028, 6, tt.DISK), (2048, 8, tt.PHANTOM), (3000, 4, tt.SPARSE),
-                                      (4096, 6, tt.DISK), (4100, 3, tt.PHANTOM), (8192, 2, tt.DISK)])
+                                      (4096, 6, tt.DISK), (4100, 3, tt.PHANTOM), (8192, 2, tt.DISK), (20000, 2, tt.DISK)])
 def test_tma_radon_equals_texture_and_replay(gpu, n, A, kind):
     img = tt.synth_image(kind, n)
     got, c, s, w = _raw(img, n, 0, A, A, sampler=2)
