@@ -20,8 +20,11 @@ for i in range(count):
                        p=[0.3, 0.5, 0.2]))
     A = int(rng.integers(1, 9)) * (2 if rng.random() < 0.8 else 1)
     kind = int(rng.choice([tt.DISK, tt.PHANTOM, tt.SPARSE]))
-    sampler = int(rng.integers(0, 2))
     full = bool(rng.random() < 0.8)
+    # samplers 0 (LDG), 1 (texture), 2 (TMA tiles for the T0 launches they serve, texture otherwise)
+    sampler = int(rng.integers(0, 3))
+    if not full and sampler == 2 and rng.random() < 0.5:  # bias T0 sizes towards the TMA kernel's range
+        n = int(rng.integers(769, 5000)) // 4 * 4
     ctx.set_sampler(sampler)
     # angle sub-ranges (a0, a_count) and image batches (trace_t05_batch) as well
     a0 = int(rng.integers(0, A)) if rng.random() < 0.2 else 0
