@@ -471,7 +471,13 @@ tt_status tt_plan_create(tt_ctx* ctx, const tt_plan_desc* d, tt_plan** out) {
     // chunks: >= ~1.6e7 unit-taps (~40 us of kernel) each so the per-chunk enqueue cost stays hidden,
     // at most 32 (measured on C2: 5 chunks 1.28 ms, 24-32 chunks 1.24 ms; C1 best unchunked)
     int ch = d->chunks;
-    if (ch == 0) ch = int(std::max(1LL, std::min(32LL, (long long)p->units * B * n * n / 16000000LL)));
+    // at most 8 for one large image (n >= 2048): its chunks are milliseconds long, the D2H of a chunk's rows
+    // hides behind the next chunk either way, and fewer chunk boundaries mean fewer partial waves
+    // (C3 e2e 34.68 ms with 32 chunks, 34.18 with 8, graph mode; scripts/plan_chunks_c3.py)
+    if (ch == 0) {
+        const long long cap = (B == 1 && n >= 2048) ? 8 : 32;
+        ch = int(std::max(1LL, std::min(cap, (long long)p->units * B * n * n / 16000000LL)));
+    }
     p->chunks = std::max(1, std::min(ch, B > 1 ? B : p->units));  // angle chunks (one image) or image chunks
     const int nslots = d->slots > 0 ? d->slots : (B > 1 ? 1 : 2);
     p->d.slots = nslots;
