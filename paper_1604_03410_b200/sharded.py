@@ -254,11 +254,16 @@ class ShardedTrace:
         return self.meds[(self.step - 1) % self.nslots] if self.rank == self.root else None
 
     def close(self) -> None:
+        """Finish outstanding steps, unmap the peers' mappings and free rank 0's exported buffers (the
+        tensors returned by ``out`` / ``med`` are invalid afterwards)."""
         self.wait()
         self.dist.barrier(group=self.group)  # no rank still writes into rank 0's buffers
         self._close()
         self.dist.barrier(group=self.group)  # every mapping closed before rank 0 frees the exported buffers
         self.outs = self.meds = []
+        for bufs in self._ipc_bufs:
+            for b in bufs:
+                b.free()
         self._ipc_bufs = ([], [])
         if self.tex is not None:
             image_texture_destroy(self.tex)

@@ -339,10 +339,16 @@ class IpcBuffer:
         return {"shape": self.shape, "typestr": self.dtype.str, "data": (self.ptr, False), "version": 3,
                 "strides": None}
 
-    def __del__(self):
+    def free(self) -> None:
         if getattr(self, "ptr", None):
             lib.tt_ipc_free(C.c_void_p(self.ptr))
             self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # interpreter shutdown: the library may already be unloaded
+            pass
 
 
 def weights_soa(wtab_ptr: int, n: int, wsoa_ptr: int, stream: int = 0) -> None:
