@@ -15,7 +15,7 @@ ctx = tt.create_context(0)
 img = torch.from_numpy(tt.synth_image(tt.DISK, n)).pin_memory()
 out = [torch.empty((A, 6, n)).pin_memory() for _ in range(2)]
 med = [torch.empty((A, 2, n), dtype=torch.int32).pin_memory() for _ in range(2)]
-for chunks in (4, 8, 16, 32):
+for chunks in [int(x) for x in os.environ.get("TT_CHUNKS", "4,8,16,32").split(",")]:
     for graph in (False, True):
         plan = tt.Plan(ctx, n, A, chunks=chunks, graph=graph)
         for i in range(2):
