@@ -134,12 +134,10 @@ static tt::TraceArgs to_args(const tt_trace_desc* d) {
     return ta;
 }
 
-// Raw-pointer launches without a prepared weight layout convert wtab into
-// stream-ordered scratch around the launch (one extra small kernel).
 // Stream-ordered scratch of the raw entries comes from the device's default pool; keep freed blocks in
 // it (once per device) so a steady stream of calls never returns memory to the driver and re-maps it
 // inside the caller's stream (measured: +0.2..3 ms per call at C2 with the default threshold of 0).
-void keep_default_pool(cudaStream_t) {
+void keep_default_pool() {
     static std::atomic<int> done[64];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || done[dev & 63].load(std::memory_order_acquire)) return;
@@ -151,6 +149,8 @@ void keep_default_pool(cudaStream_t) {
     done[dev & 63].store(1, std::memory_order_release);
 }
 
+// Raw-pointer launches without a prepared weight layout convert wtab into
+// stream-ordered scratch around the launch (one extra small kernel).
 struct WeightScratch {
     float* d = nullptr;
     cudaStream_t s = nullptr;
@@ -159,7 +159,7 @@ struct WeightScratch {
     }
     cudaError_t prepare(tt::TraceArgs& ta, cudaStream_t stream) {
         if (!ta.full || ta.wsoa) return cudaSuccess;
-        keep_default_pool(stream);
+        keep_default_pool();
         s = stream;
         cudaError_t e = cudaMallocAsync((void**)&d, tt::weights_soa_bytes(ta.n), stream);
         if (e != cudaSuccess) return e;
@@ -177,7 +177,7 @@ struct CounterScratch {
     }
     cudaError_t prepare(tt::TraceArgs& ta, cudaStream_t stream) {
         if (!ta.circ || !ta.fuse_circus) return cudaSuccess;
-        keep_default_pool(stream);
+        keep_default_pool();
         s = stream;
         const std::size_t bytes = tt::epi_state_ints(ta) * sizeof(int);
         cudaError_t e = cudaMallocAsync((void**)&d, bytes, stream);
@@ -826,7 +826,12 @@ tt_status tt_ipc_alloc(int device, size_t bytes, void** d_ptr) {
     cudaError_t e = cudaMalloc(d_ptr, bytes);
     if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMalloc (IPC buffer)");
     e = cudaMemset(*d_ptr, 0, bytes);
-    return e == cudaSuccess ? TT_OK : cuda_fail(nullptr, e, "cudaMemset (IPC buffer)");
+    if (e != cudaSuccess) {
+        cudaFree(*d_ptr);
+        *d_ptr = nullptr;
+        return cuda_fail(nullptr, e, "cudaMemset (IPC buffer)");
+    }
+    return TT_OK;
 }
 
 tt_status tt_ipc_free(void* d_ptr) {
