@@ -166,7 +166,7 @@ tt_status tt_ctx_stream(tt_ctx* ctx, void** stream_out); /* cudaStream_t for int
 tt_status tt_ctx_device(const tt_ctx* ctx, int* device_out);
 /* Extension: image sampler of this context's trace launches:
  * 0 = global/L1 loads, 1 = texture gather (TLD4) for every launch, 2 (default) =
- * TMA-staged shared-memory tiles for the T0-only launches they serve (n > 768,
+ * TMA-staged shared-memory tiles for the T0-only launches they serve (n > 704,
  * n % 4 == 0, one image) and the texture gather for every other launch -- the
  * measured-faster sampler for each.  Plans always sample through
  * their texture unless the sampler is 0. */
@@ -246,7 +246,7 @@ tt_status tt_tld4_probe(unsigned* d_out, int blocks, int iters, void* stream);
  * default).  out: full ? [a_count][6][n] : [a_count][n]; med may be NULL.
  * sampler: 0 = global/L1 loads, 1 = texture gather through a cudaArray copy of
  * img that this call makes, 2 = TMA-staged shared-memory tiles read straight
- * from img (T0 only, 768 < n with a 32-lane schedule, n % 4 == 0, batch 1, img 16-B aligned; other
+ * from img (T0 only, 704 < n with a 32-lane schedule, n % 4 == 0, batch 1, img 16-B aligned; other
  * launches fall back to 1); all are asynchronous (the call only enqueues):
  * the copy is released once its launch has completed (recorded event, reclaimed
  * by later calls and at exit).  Repeated texture launches on one image should

@@ -20,7 +20,7 @@ constexpr int kNumF = 6;  // T0..T5
 enum class Sampler : int {
     Global = 0,   // 4 x LDG through L1 (row-major image in HBM/L2)
     Texture = 1,  // 1 x TLD4 (tex2Dgather) on a block-linear cudaArray copy
-    Tma = 2,      // T0 only (n > 768, NS = 32, n % 4 == 0, one image): TMA-staged shared-memory tiles, 4 x LDS;
+    Tma = 2,      // T0 only (n > 704, NS = 32, n % 4 == 0, one image): TMA-staged shared-memory tiles, 4 x LDS;
                   // other launches fall back to Texture (tex must then be set; tma_radon_ok())
 };
 

@@ -87,7 +87,7 @@ class ShardedTrace:
         self.device = torch.device("cuda", device)
         if sampler is None:  # the measured-faster sampler: TMA tiles for the T0 launches they serve, else texture
             from .trace import schedule_slots
-            tma = not full and n > 768 and n % 4 == 0 and schedule_slots(n, False) == 32
+            tma = not full and n > 704 and n % 4 == 0 and schedule_slots(n, False) == 32
             sampler = 2 if tma else 1
         self.sampler = sampler
         dev = self.device

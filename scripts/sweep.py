@@ -83,7 +83,7 @@ def main():
                 if full and n > tt.max_full_n():
                     continue
                 reps = 5 if n * n * A > 4e10 else 10
-                tma_ok = not full and n > 768 and n % 4 == 0  # the product rule for these (power-of-two) n
+                tma_ok = not full and n > 704 and n % 4 == 0  # the product rule for these (power-of-two) n
                 smp = 2 if (args.sampler == "tma" or (args.sampler == "auto" and tma_ok)) else 1
                 pt = run_point(n, A, full, stream, flush, reps, peak, tpeak, smp)
                 pt["fp32_peak_tflops"] = peak

@@ -3,7 +3,7 @@
 The tile kernel keeps the texture kernel's per-tap arithmetic, slot order and
 butterfly, so its sinogram must equal the texture path's bit for bit, and the
 oracle's replay of the NS = 32 schedule (TTO_REPLAY); launches it does not
-serve (T0-T5, n <= 768, n % 4 != 0) fall back to the texture gather.
+serve (T0-T5, n <= 704, n % 4 != 0) fall back to the texture gather.
 """
 import numpy as np
 import pytest
@@ -92,7 +92,7 @@ def test_tma_radon_unmirrored_partner(gpu):
     assert _bitwise_equal(outs[0], rout)
 
 
-@pytest.mark.parametrize("n,full", [(512, False), (768, False), (1030, False), (2048, True)])
+@pytest.mark.parametrize("n,full", [(512, False), (704, False), (1030, False), (2048, True)])
 def test_tma_sampler_falls_back_to_texture(gpu, n, full):
     """Launches the tile kernel does not serve run the texture gather (same bits as sampler 1)."""
     A = 4
