@@ -269,7 +269,8 @@ def run_ours(args, ws, rank, local):
     if orient:
         # the multi-GPU public call: shard kernels write rows into rank 0's sinogram over NVLink P2P,
         # per-chunk completion signals; the device leg starts with the image already on every GPU
-        st = ShardedTrace(n, A, dist, local, full=full, chunks=args.chunks or 4, sampler=args.sampler)
+        st = ShardedTrace(n, A, dist, local, full=full, chunks=args.chunks or 4, sampler=args.sampler,
+                          assembly=args.assembly)  # falls back to "gather" if the IPC mapping fails
         st.img[0].copy_(torch.from_numpy(img_h[0]))
         torch.cuda.synchronize()
         stream = st.stream
@@ -386,10 +387,16 @@ def run_ours(args, ws, rank, local):
         nb_img = n * n * 4 if root else 0
         d2h = A * (F + (2 if full else 0)) * n * 4 if root else 0
         chunks_note = f"{st.chunks} chunks per shard"
-        api = (f"ShardedTrace.submit/wait (per step: rank 0 pinned H2D of the image, NCCL broadcast, "
-               f"{chunks_note} of fused-kernel launches writing rows into rank 0's sinogram over NVLink P2P, "
-               f"a 4-byte completion all_reduce per chunk, rank 0 D2H of sinogram + medians overlapped "
-               f"chunk by chunk)")
+        if st.assembly == "p2p":
+            api = (f"ShardedTrace.submit/wait (per step: rank 0 pinned H2D of the image, NCCL broadcast, "
+                   f"{chunks_note} of fused-kernel launches writing rows into rank 0's sinogram over NVLink P2P, "
+                   f"a 4-byte completion all_reduce per chunk, rank 0 D2H of sinogram + medians overlapped "
+                   f"chunk by chunk)")
+        else:
+            api = (f"ShardedTrace(assembly='gather').submit/wait (per step: rank 0 pinned H2D of the image, "
+                   f"NCCL broadcast, {chunks_note} of fused-kernel launches into a local shard block, one NCCL "
+                   f"all-gather of every shard, rank 0 reorders into angle order and downloads sinogram + "
+                   f"medians)")
     else:
         ctx = tt.create_context(local)
         ctx.set_sampler(args.sampler)
@@ -533,8 +540,10 @@ def run_ours(args, ws, rank, local):
                        "images": batch_total if images else (1 if orient else ws),
                        "functionals": ("T0-T5" if full else "T0") + (" + P1-P3 circus" if feats_on else ""),
                        "sampler": ["ldg", "tex"][args.sampler],
-                       "parallelism": (f"orientations sharded x{ws}; fused kernels write sinogram rows into "
-                                       "rank 0 over NVLink P2P + per-chunk 4-byte NCCL completion signal"
+                       "parallelism": ((f"orientations sharded x{ws}; fused kernels write sinogram rows into "
+                                        "rank 0 over NVLink P2P + per-chunk 4-byte NCCL completion signal"
+                                        if st.assembly == "p2p" else
+                                        f"orientations sharded x{ws}; one NCCL all-gather of the shards per step")
                                        if orient else
                                        (f"images sharded x{ws} + NCCL feature gather" if images and ws > 1 else
                                         (f"one image per rank x{ws} + NCCL feature gather" if ws > 1 else
@@ -649,6 +658,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sampler", type=int, default=int(os.environ.get("TT_BENCH_SAMPLER", "1")), choices=[0, 1])
     ap.add_argument("--chunks", type=int, default=0, help="angle chunks per shard (orientation sharding; 0: 4)")
+    ap.add_argument("--assembly", default="p2p", choices=["p2p", "gather"],
+                    help="orientation sharding: shard rows stored into rank 0 over P2P (default) or one NCCL "
+                         "all-gather per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dev-one-gpu", action="store_true",
                     help="validation only: every rank on cuda:0 with gloo (exercises the multi-rank data path, "

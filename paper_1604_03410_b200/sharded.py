@@ -26,6 +26,14 @@ after that broadcast, so no rank overwrites rows that are still being read.
 every GPU): the device-resident leg of bench.py.  Results equal one
 single-GPU launch bit-for-bit (tests/test_sharded_gpu.py).
 
+``assembly="gather"`` is the north_star's literal form of step 3-4: every
+rank's kernels write its shard into a local [2cnt] block (forward rows, then
+mirror rows), ONE all-gather (NCCL over NVLink) of the flat out+median block
+per step brings every shard to rank 0, which reorders them into angle order on
+the device and downloads the whole sinogram.  It needs equal shards
+((A/2) % G == 0).  It is also the fallback when the CUDA IPC mapping of rank
+0's buffers fails (no peer access between two of the GPUs).
+
 Failure detection: every collective is issued asynchronously and its Work
 kept; ``check()`` (called by ``wait``) raises the first communicator error
 (NCCL async errors surface through torch's watchdog when
@@ -75,7 +83,7 @@ class ShardedTrace:
     Outputs on rank 0: ``out`` [A][F][n] f32 and ``med`` [A][2][n] i32."""
 
     def __init__(self, n: int, angles: int, dist, device: int, full: bool = True, chunks: int = 4,
-                 sampler: int | None = None, group=None, root: int = 0, slots: int = 2):
+                 sampler: int | None = None, group=None, root: int = 0, slots: int = 2, assembly: str = "p2p"):
         import torch
 
         self.torch, self.dist, self.group, self.root = torch, dist, group, root
@@ -103,22 +111,57 @@ class ShardedTrace:
             self.signal = [torch.zeros(1, device=dev) for _ in range(self.chunks)]
             is_root = self.rank == root
             self.slots = slots if is_root else 0
-            # exported buffers are dedicated allocations (IpcBuffer), not caching-allocator blocks
-            self._ipc_bufs = ([IpcBuffer(device, (angles, self.F, n), "float32") for _ in range(self.slots)],
-                              [IpcBuffer(device, (angles, 2, n), "int32") for _ in range(self.slots)])
-            self.outs = [torch.as_tensor(b, device=dev) for b in self._ipc_bufs[0]]
-            self.meds = [torch.as_tensor(b, device=dev) for b in self._ipc_bufs[1]]
+            if assembly not in ("p2p", "gather"):
+                raise ValueError(f"assembly must be 'p2p' or 'gather', not {assembly!r}")
+            self._ipc_bufs = ([], [])
+            if assembly == "p2p":
+                # exported buffers are dedicated allocations (IpcBuffer), not caching-allocator blocks
+                self._ipc_bufs = ([IpcBuffer(device, (angles, self.F, n), "float32") for _ in range(self.slots)],
+                                  [IpcBuffer(device, (angles, 2, n), "int32") for _ in range(self.slots)])
+                self.outs = [torch.as_tensor(b, device=dev) for b in self._ipc_bufs[0]]
+                self.meds = [torch.as_tensor(b, device=dev) for b in self._ipc_bufs[1]]
         if full:
             weights_soa(self.wtab.data_ptr(), n, self.wsoa.data_ptr(), self.stream.cuda_stream)
         self.tex = image_texture(self.img[0].data_ptr(), n, self.stream.cuda_stream) if sampler == 1 else None
         self.stream.synchronize()
-        # rank 0's output slots, mapped into every rank (CUDA IPC; NVLink peer access across GPUs)
-        ptrs = [p for o, m in zip(self.outs, self.meds) for p in (o.data_ptr(), m.data_ptr())]
         nslots = [slots]
         dist.broadcast_object_list(nslots, src=root, group=group)
         self.nslots = nslots[0]
-        self.peer, self._close = shard.share_device_buffers(ptrs if is_root else [], dist, device, src=root,
-                                                            group=group)
+        self.peer, self._close = [], (lambda: None)
+        if assembly == "p2p":
+            # rank 0's output slots, mapped into every rank (CUDA IPC; NVLink peer access across GPUs)
+            ptrs = [p for o, m in zip(self.outs, self.meds) for p in (o.data_ptr(), m.data_ptr())]
+            try:
+                self.peer, self._close = shard.share_device_buffers(ptrs if is_root else [], dist, device, src=root,
+                                                                    group=group)
+                ok = 1
+            except Exception:  # e.g. no peer access between two of the GPUs
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            if int(flag.item()) == 0:  # every rank agrees: fall back to the gather assembly
+                self._close()
+                self.peer, self._close = [], (lambda: None)
+                self.outs = self.meds = []
+                for bufs in self._ipc_bufs:
+                    for b in bufs:
+                        b.free()
+                self._ipc_bufs = ([], [])
+                assembly = "gather"
+        self.assembly = assembly
+        if assembly == "gather":
+            h, G = angles // 2, self.world
+            if h % G:
+                raise ValueError("the gather assembly needs equal shards: (angles/2) % world == 0")
+            rows = 2 * self.cnt
+            self._nout = rows * self.F * n                 # f32 words of the local sinogram block
+            self._nblk = self._nout + (rows * 2 * n if full else 0)  # + the i32 median block (same buffer)
+            with torch.cuda.stream(self.stream):
+                self.loc = torch.empty(self._nblk, device=dev)          # this rank's [2cnt] rows, flat
+                self.raw = torch.empty((G, self._nblk), device=dev)    # every rank's block (all-gather target)
+                self.outs = [torch.empty((angles, self.F, n), device=dev) for _ in range(self.slots)]
+                self.meds = [torch.empty((angles, 2, n), dtype=torch.int32, device=dev) for _ in range(self.slots)]
+            self.stream.synchronize()
         self.step = 0
         self._works = []
         self.copy_done = [None] * self.nslots
@@ -130,14 +173,47 @@ class ShardedTrace:
         if u1 <= u0:
             return
         F, n = self.F, self.n
-        row = self.a0 + u0  # forward rows; mirror rows at partner_row = A/2 further on
-        out_ptr = self.peer[2 * slot] + row * F * n * 4
-        med_ptr = self.peer[2 * slot + 1] + row * 2 * n * 4 if self.full else 0
+        if self.assembly == "p2p":
+            row = self.a0 + u0  # forward rows; mirror rows at partner_row = A/2 further on
+            out_ptr = self.peer[2 * slot] + row * F * n * 4
+            med_ptr = self.peer[2 * slot + 1] + row * 2 * n * 4 if self.full else 0
+            partner, peer = self.h, self.rank != self.root
+        else:  # local [2cnt] block: forward rows u0.., mirror rows cnt + u0..
+            out_ptr = self.loc.data_ptr() + u0 * F * n * 4
+            med_ptr = self.loc.data_ptr() + (self._nout + u0 * 2 * n) * 4 if self.full else 0
+            partner, peer = self.cnt, False
         trace_device(self.img[k].data_ptr(), n, self.a0 + u0, 2 * (u1 - u0), self.ctab.data_ptr(),
                      self.stab.data_ptr(), self.wtab.data_ptr(), out_ptr, med_ptr, full=self.full,
                      sampler=self.sampler, stream=self.stream.cuda_stream, tex=self.tex, pair_stride=self.h,
-                     wsoa_ptr=self.wsoa.data_ptr() if self.full else 0, partner_row=self.h,
-                     peer_out=self.rank != self.root)
+                     wsoa_ptr=self.wsoa.data_ptr() if self.full else 0, partner_row=partner,
+                     peer_out=peer)
+
+    def _gather(self, slot: int, host_out=None, host_med=None) -> None:
+        """Gather assembly: one all-gather of every rank's flat block, rank 0 reorders the rows into
+        angle order (``shard.assemble``) and downloads the whole sinogram."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            if self.dist.get_backend(self.group) == "nccl":
+                w = self.dist.all_gather_into_tensor(self.raw, self.loc, group=self.group, async_op=True)
+            else:  # gloo: the list form
+                w = self.dist.all_gather(list(self.raw.unbind(0)), self.loc, group=self.group, async_op=True)
+            w.wait()
+            self._works.append(w)
+            if self.rank != self.root:
+                return
+            G, cnt, F, n = self.world, self.cnt, self.F, self.n
+            self.outs[slot].copy_(self.raw[:, :self._nout].reshape(G, 2, cnt, F, n).transpose(0, 1)
+                                  .reshape(self.A, F, n))
+            if self.full:
+                self.meds[slot].copy_(self.raw[:, self._nout:].view(torch.int32).reshape(G, 2, cnt, 2, n)
+                                      .transpose(0, 1).reshape(self.A, 2, n))
+        if host_out is not None or host_med is not None:
+            self.copy_stream.wait_stream(self.stream)
+            with torch.cuda.stream(self.copy_stream):
+                if host_out is not None:
+                    host_out.copy_(self.outs[slot], non_blocking=True)
+                if host_med is not None and self.full:
+                    host_med.copy_(self.meds[slot], non_blocking=True)
 
     def _signal(self, c: int) -> None:
         """Chunk c of every shard has landed in rank 0's buffers once this all_reduce completes
@@ -164,6 +240,15 @@ class ShardedTrace:
         torch = self.torch
         if self.tex is not None:
             image_texture_update(self.tex, self.img[k].data_ptr(), 0, self.stream.cuda_stream)
+        if self.assembly == "gather":
+            for c in range(self.chunks):
+                self._launch(slot, k, c)
+            self._gather(slot, host_out, host_med)
+            if self.rank == self.root:
+                ev = torch.cuda.Event()
+                ev.record(self.copy_stream)
+                self.copy_done[slot] = ev
+            return
         for c in range(self.chunks):
             self._launch(slot, k, c)
             self._signal(c)

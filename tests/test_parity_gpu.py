@@ -166,6 +166,25 @@ def test_unpaired_raw_launch_matches_unpaired_replay(ctx):
     assert fails == 0, st
 
 
+@pytest.mark.parametrize("n", [64, 255, 512, 700])
+def test_clipped_t0_off_grid_and_near_axis_angles(ctx, n):
+    """Texture T0 launches sample only the tap range that can lie inside the image
+    (clip_range, a superset solved with a 2-pixel margin): off-grid angles, angles a
+    few ulps from the axes (direction cosines below the 2^-20 cut-off, and just
+    above it) and exact axes must give the replay's bits, which walks every tap."""
+    rng = np.random.default_rng(n)
+    th = np.concatenate([rng.uniform(0, 2 * np.pi, 10),
+                         [0.0, np.pi / 2, np.pi, 1e-7, np.pi / 2 + 3e-7, 2.0 ** -19, 2.0 ** -21, np.pi / 4,
+                          -2.0 ** -20 + np.pi]])
+    c = np.cos(th).astype(np.float32)
+    s = np.sin(th).astype(np.float32)
+    _, _, w = tt.make_tables(n, 2)
+    img = tt.synth_image(tt.PHANTOM, n) + np.float32(0.25)  # non-zero up to the image border
+    out, _ = _raw(ctx, img, n, c, s, w, 0, len(th), -1, full=False, sampler=1)
+    ro, _ = O.replay_launch(img, n, c, s, w, a0=0, units=len(th), pair_stride=0, full=False)
+    assert _bitwise_equal(out, ro)
+
+
 def test_zero_image_gives_zero_functionals_and_zero_medians(ctx):
     n, A = 64, 6
     img = np.zeros((n, n), np.float32)

@@ -4,7 +4,9 @@ stores -- the same mechanism as peer access over NVLink between GPUs): the
 host-to-host path (rank 0 upload + broadcast, chunked shard kernels writing
 into rank 0's sinogram, per-chunk signals, chunked downloads) and the
 device-resident path must both equal one single-GPU launch bit for bit, over
-several consecutive overlapped submissions."""
+several consecutive overlapped submissions.  The same with assembly="gather"
+(local shard blocks + one all-gather per step, the north_star's NCCL-gather
+form and the fallback when the IPC mapping fails)."""
 import os
 import socket
 
@@ -21,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, A, chunks, result, full=True):
+def _worker(rank, world, port, n, A, chunks, result, full=True, assembly="p2p"):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -33,10 +35,10 @@ def _worker(rank, world, port, n, A, chunks, result, full=True):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     F = 6 if full else 1
-    st = ShardedTrace(n, A, dist, 0, chunks=chunks, full=full)  # T0 at n > 768: the TMA tile kernel
+    st = ShardedTrace(n, A, dist, 0, chunks=chunks, full=full, assembly=assembly)  # T0 at n > 768: TMA tiles
+    ok = st.assembly == assembly
     imgs = [tt.synth_image(kind, n) for kind in (tt.PHANTOM, tt.DISK, tt.SPARSE)]
     root = rank == 0
-    ok = True
     hi = [torch.from_numpy(im).pin_memory() for im in imgs] if root else [None] * 3
     ho = [torch.full((A, F, n), float("nan")).pin_memory() for _ in imgs] if root else [None] * 3
     hm = [torch.full((A, 2, n), -1, dtype=torch.int32).pin_memory() for _ in imgs] if root else [None] * 3
@@ -69,15 +71,17 @@ def _worker(rank, world, port, n, A, chunks, result, full=True):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,A,chunks,full", [(2, 256, 40, 3, True), (4, 512, 24, 2, True), (3, 128, 18, 4, True),
-                                                   (2, 1024, 16, 2, False)])
-def test_sharded_trace_equals_one_launch(gpu, world, n, A, chunks, full):
+@pytest.mark.parametrize("world,n,A,chunks,full,assembly", [
+    (2, 256, 40, 3, True, "p2p"), (4, 512, 24, 2, True, "p2p"), (3, 128, 18, 4, True, "p2p"),
+    (2, 1024, 16, 2, False, "p2p"),
+    (2, 256, 40, 3, True, "gather"), (4, 512, 24, 2, True, "gather"), (2, 1024, 16, 2, False, "gather")])
+def test_sharded_trace_equals_one_launch(gpu, world, n, A, chunks, full, assembly):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, A, chunks, q, full)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, A, chunks, q, full, assembly)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
