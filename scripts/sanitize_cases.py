@@ -42,13 +42,24 @@ for n, A, pair in [(256, 12, 0), (2048, 4, 0), (256, 16, 8)]:
     hp = torch.empty((A * 6, 4), dtype=torch.float64, device="cuda")
     cen = torch.empty(A * 6, dtype=torch.int32, device="cuda")
     tt.hermite_device(out.data_ptr(), n, A * 6, 4, hp.data_ptr(), cen.data_ptr())
-for n, A, a0, pair in [(1028, 6, 0, 0), (2052, 5, 0, 0), (2048, 8, 2, 8)]:
+for n, A, a0, pair in [(1028, 6, 0, 0), (2052, 5, 0, 0), (2048, 8, 2, 8), (2048, 12, 0, 0), (4096, 8, 0, 0)]:
     c, s, w = tt.make_tables(n, 16 if pair else A)
     d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
     img, ct, st, wt = d(tt.synth_image(tt.SPARSE, n)), d(c), d(s), d(w)
     out = torch.empty((A if not pair else 8, n), device="cuda")
     tt.trace_device(img.data_ptr(), n, a0, A if not pair else 8, ct.data_ptr(), st.data_ptr(), wt.data_ptr(),
                     out.data_ptr(), 0, full=False, sampler=2, pair_stride=pair)
+# texture T0 launches over the clipped tap range (NS >= 16), off-axis angles
+for n, A in [(512, 12), (640, 8)]:
+    c, s, w = tt.make_tables(n, A)
+    d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    img, ct, st, wt = d(tt.synth_image(tt.PHANTOM, n)), d(c), d(s), d(w)
+    out = torch.empty((A, n), device="cuda")
+    tex = tt.trace.image_texture(img.data_ptr(), n)
+    tt.trace_device(img.data_ptr(), n, 0, A, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(), 0,
+                    full=False, sampler=1, tex=tex)
+    torch.cuda.synchronize()
+    tt.trace.image_texture_destroy(tex)
 frame = torch.empty((90, 90), device="cuda")
 pic = torch.rand((40, 50), device="cuda")
 tt.orthonormal_device(pic.data_ptr(), 40, 50, 90, frame.data_ptr())
