@@ -85,7 +85,7 @@ void drop_texture(tt_ctx* ctx, std::uint64_t base) {
     if (it == ctx->tex_cache.end()) return;
     cudaStreamSynchronize(ctx->stream);
     cudaDestroyTextureObject(it->second.tex);
-    cudaFreeArray(it->second.arr);
+    if (it->second.arr) cudaFreeArray(it->second.arr);
     ctx->tex_cache.erase(it);
 }
 
@@ -394,11 +394,12 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     if (ta.sampler == tt::Sampler::Tma && !tt::tma_radon_ok(ta)) ta.sampler = tt::Sampler::Texture;
     if (ta.sampler == tt::Sampler::Texture) {
         TexEntry& te = ctx.tex_cache[img.base];
-        if (te.arr == nullptr || te.n != n || te.batch != batch) {
-            if (te.arr) {
+        const bool view = te.tex != 0 && te.arr == nullptr;  // pitch-linear view of the allocation (small n)
+        if (te.tex == 0 || te.n != n || te.batch != batch || (view && te.bound != ta.img)) {
+            if (te.tex) {
                 cudaStreamSynchronize(ctx.stream);
                 cudaDestroyTextureObject(te.tex);
-                cudaFreeArray(te.arr);
+                if (te.arr) cudaFreeArray(te.arr);
                 te = TexEntry{};
             }
             cudaError_t e = batch > 1 ? tt::make_image_atlas(ta.img, n, batch, (long long)N * N, ctx.stream, &te.arr,
@@ -411,7 +412,8 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
             te.n = n;
             te.batch = batch;
             te.gen = img.gen;
-        } else if (te.gen != img.gen || img.exported) {  // image (maybe) rewritten since the copy: refresh
+            te.bound = ta.img;
+        } else if (!view && (te.gen != img.gen || img.exported)) {  // image (maybe) rewritten since the copy: refresh
             cudaError_t e = batch > 1 ? tt::fill_image_atlas(te.arr, ta.img, n, batch, (long long)N * N, te.cols,
                                                               ctx.stream)
                                       : cudaMemcpy2DToArrayAsync(te.arr, 0, 0, ta.img, std::size_t(n) * 4,

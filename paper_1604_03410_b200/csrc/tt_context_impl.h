@@ -112,8 +112,9 @@ struct TexEntry {
     int n = 0;
     int batch = 1;
     int cols = 1;
-    cudaArray_t arr = nullptr;
+    cudaArray_t arr = nullptr;     // null: a pitch-linear view of the image (nothing to refresh)
     cudaTextureObject_t tex = 0;
+    const float* bound = nullptr;  // the image pointer the texture was made from
 };
 
 // Pass-2 weight layout (tt::launch_weights_soa) cached per wtab allocation,

@@ -36,7 +36,7 @@ std::vector<DeferredTex> g_tex_pending;
 void release(const DeferredTex& t) {
     DeviceGuard guard(t.device);
     cudaDestroyTextureObject(t.tex);
-    cudaFreeArray(t.arr);
+    if (t.arr) cudaFreeArray(t.arr);
     cudaEventDestroy(t.done);
 }
 
@@ -244,11 +244,12 @@ tt_status tt_trace_device(const tt_trace_desc* d, void* stream) {
 }  // extern "C"
 
 struct tt_image_tex {
-    cudaArray_t arr = nullptr;
+    cudaArray_t arr = nullptr;  // null: pitch-linear views of images (small n), one per image pointer seen
     cudaTextureObject_t tex = 0;
     int n = 0;
     int batch = 1;
     int cols = 1;
+    std::vector<std::pair<const float*, cudaTextureObject_t>> views;  // (image, view); tex is one of them
 };
 
 extern "C" {
@@ -291,6 +292,7 @@ tt_status tt_image_tex_create(const float* d_img, int n, void* stream, tt_image_
         if (t->arr) cudaFreeArray(t->arr);
         return cuda_fail(nullptr, e, "make_image_texture");
     }
+    if (!t->arr) t->views.emplace_back(d_img, t->tex);
     *out = t.release();
     return TT_OK;
 }
@@ -315,6 +317,21 @@ tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, std::int64_t
     if (!t || !d_imgs) return fail(nullptr, TT_ERR_INVALID, "bad argument");
     const long long stride = img_stride > 0 ? img_stride : (long long)t->n * t->n;
     cudaError_t e;
+    if (!t->arr) {  // a view: launches read the image itself; another image gets (or reuses) its own view
+        for (const auto& v : t->views)
+            if (v.first == d_imgs) {
+                t->tex = v.second;
+                return TT_OK;
+            }
+        if (!tt::pitch_texture_ok(d_imgs, t->n)) return fail(nullptr, TT_ERR_INVALID, "image not texture-aligned");
+        cudaArray_t none = nullptr;
+        cudaTextureObject_t tex = 0;
+        e = tt::make_image_texture(d_imgs, t->n, (cudaStream_t)stream, &none, &tex);
+        if (e != cudaSuccess) return cuda_fail(nullptr, e, "image texture view");
+        t->views.emplace_back(d_imgs, tex);  // kept until destroy: earlier launches may still use the others
+        t->tex = tex;
+        return TT_OK;
+    }
     if (t->batch == 1 && t->cols == 1)
         e = cudaMemcpy2DToArrayAsync(t->arr, 0, 0, d_imgs, std::size_t(t->n) * 4, std::size_t(t->n) * 4,
                                      std::size_t(t->n), cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
@@ -325,8 +342,12 @@ tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, std::int64_t
 
 tt_status tt_image_tex_destroy(tt_image_tex* t) {
     if (!t) return TT_OK;
-    cudaDestroyTextureObject(t->tex);
-    cudaFreeArray(t->arr);
+    if (t->views.empty()) {
+        cudaDestroyTextureObject(t->tex);
+    } else {
+        for (const auto& v : t->views) cudaDestroyTextureObject(v.second);
+    }
+    if (t->arr) cudaFreeArray(t->arr);
     delete t;
     return TT_OK;
 }
@@ -651,7 +672,7 @@ tt_status tt_plan_submit(tt_plan* p, const float* h_img, float* h_out, std::int3
     };
     if (B == 1) {
         // 1. image in on the upload stream (straight into the texture array when the sampler reads it)
-        if (tex)
+        if (tex && sl.arr)
             ok(cudaMemcpy2DToArrayAsync(sl.arr, 0, 0, h_img, std::size_t(n) * 4, std::size_t(n) * 4, std::size_t(n),
                                         cudaMemcpyHostToDevice, p->si));
         else

@@ -105,6 +105,8 @@ cudaError_t launch_copy_f32(const float* a, float* b, uint64_t count, cudaStream
 cudaError_t launch_add_to_f32(const float* in, float* out, uint64_t count, cudaStream_t s);
 
 // Texture object over a cudaArray holding a copy of img (caller owns both).
+// true when make_image_texture makes a pitch-linear view of img (no cudaArray: *arr == nullptr)
+bool pitch_texture_ok(const float* img, int n);
 cudaError_t make_image_texture(const float* img, int n, cudaStream_t s, cudaArray_t* arr,
                                cudaTextureObject_t* tex);
 

@@ -451,7 +451,9 @@ def image_atlas(imgs_ptr: int, n: int, batch: int, img_stride: int = 0, stream: 
 
 
 def image_texture_update(t, imgs_ptr: int, img_stride: int = 0, stream: int = 0) -> None:
-    """Refresh a texture/atlas from device images (stream-ordered copy)."""
+    """Refresh a texture/atlas from device images (stream-ordered copy).  Small images (n <= 256) are
+    gathered through a pitch-linear view of the image itself: nothing is copied, and a different image
+    pointer switches the handle to that image's view."""
     _check(lib.tt_image_tex_update(t, C.c_void_p(imgs_ptr), img_stride, C.c_void_p(stream)))
 
 

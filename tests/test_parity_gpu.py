@@ -185,6 +185,35 @@ def test_clipped_t0_off_grid_and_near_axis_angles(ctx, n):
     assert _bitwise_equal(out, ro)
 
 
+@pytest.mark.parametrize("n", [64, 256, 512])
+def test_texture_handle_follows_images(ctx, n):
+    """A texture handle refreshed from alternating device images (pitch-linear views for n <= 256,
+    array copies above) samples whichever image it was last pointed at, and the in-place rewrite of an
+    image is seen by the next launch."""
+    import torch
+
+    c, s, w = tt.make_tables(n, 8)
+    d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    imgs = [d(tt.synth_image(k, n)) for k in (tt.PHANTOM, tt.DISK)]
+    ct, st, wt = d(c), d(s), d(w)
+    tex = tt.trace.image_texture(imgs[0].data_ptr(), n)
+    try:
+        for step, k in enumerate([0, 1, 0, 1]):
+            if step == 2:
+                imgs[0].mul_(0.5)  # rewritten in place between launches
+            tt.trace.image_texture_update(tex, imgs[k].data_ptr())
+            out = torch.empty((8, 6, n), device="cuda")
+            med = torch.empty((8, 2, n), dtype=torch.int32, device="cuda")
+            tt.trace_device(imgs[k].data_ptr(), n, 0, 8, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
+                            med.data_ptr(), sampler=1, tex=tex, pair_stride=-1)
+            torch.cuda.synchronize()
+            host = imgs[k].cpu().numpy()
+            ro, rm = O.replay_launch(host, n, c, s, w, a0=0, units=8, pair_stride=0)
+            assert _bitwise_equal(out.cpu().numpy(), ro) and np.array_equal(med.cpu().numpy(), rm), (step, k)
+    finally:
+        tt.trace.image_texture_destroy(tex)
+
+
 def test_zero_image_gives_zero_functionals_and_zero_medians(ctx):
     n, A = 64, 6
     img = np.zeros((n, n), np.float32)
