@@ -165,11 +165,13 @@ tt_status tt_ctx_synchronize(tt_ctx* ctx);
 tt_status tt_ctx_stream(tt_ctx* ctx, void** stream_out); /* cudaStream_t for interop */
 tt_status tt_ctx_device(const tt_ctx* ctx, int* device_out);
 /* Extension: image sampler of this context's trace launches:
- * 0 = global/L1 loads, 1 = texture gather (TLD4) for every launch, 2 (default) =
+ * 0 = global/L1 loads, 1 = texture gather (TLD4) for every launch, 2 =
  * TMA-staged shared-memory tiles for the T0-only launches they serve (n > 704,
- * n % 4 == 0, one image) and the texture gather for every other launch -- the
- * measured-faster sampler for each.  Plans always sample through
- * their texture unless the sampler is 0. */
+ * n % 4 == 0, one image) and the texture gather for every other launch, 3
+ * (default) = as 2 for T0 launches of at least 1.5e8 taps (units * n^2), whose
+ * per-launch cost the tiles amortise, the texture gather otherwise -- the
+ * measured-faster sampler for each.  Every sampler gives the same
+ * bits.  Plans always sample through their texture unless the sampler is 0. */
 tt_status tt_ctx_set_sampler(tt_ctx* ctx, int sampler);
 
 /* ---- modules and functions (driver.hpp:138-177) ------------------------------ */

@@ -260,7 +260,8 @@ class DeviceContext:
         return out.value or 0
 
     def set_sampler(self, sampler: int) -> None:
-        """0 = global/L1 loads, 1 = texture gather (trace kernels only)."""
+        """0 = global/L1 loads, 1 = texture gather, 2 = TMA tiles for the T0 launches they serve, 3 (default)
+        = TMA tiles for T0 launches of >= 1.5e8 taps, the texture gather otherwise (trace kernels only)."""
         _check(lib.tt_ctx_set_sampler(self._p, int(sampler)), self._p)
 
     def synchronize(self) -> None:

@@ -390,8 +390,9 @@ LaunchOutcome run_trace_common(tt_ctx& ctx, const tt_grid& g, const ResolvedArg&
     ta.med = med ? (std::int32_t*)med->dptr : nullptr;
     ta.full = full;
     ta.batch = batch;
-    ta.sampler = tt::Sampler(ctx.sampler);
-    if (ta.sampler == tt::Sampler::Tma && !tt::tma_radon_ok(ta)) ta.sampler = tt::Sampler::Texture;
+    ta.sampler = tt::Sampler(ctx.sampler == 3 ? 2 : ctx.sampler);  // 3 (auto): tiles only where they pay
+    if (ta.sampler == tt::Sampler::Tma && !(ctx.sampler == 3 ? tt::tma_radon_pays(ta) : tt::tma_radon_ok(ta)))
+        ta.sampler = tt::Sampler::Texture;
     if (ta.sampler == tt::Sampler::Texture) {
         TexEntry& te = ctx.tex_cache[img.base];
         const bool view = te.tex != 0 && te.arr == nullptr;  // pitch-linear view of the allocation (small n)
@@ -676,7 +677,7 @@ tt_status tt_ctx_create(int device, const tt_caps* caps, tt_ctx** out) {
     // Default sampler 2: TMA-staged tiles for the T0 (Radon) launches they serve, the texture gather for
     // everything else -- the faster of the two for each (measured, profiles/r02_tma_radon.txt);
     // TT_SAMPLER=ldg selects L1 loads, TT_SAMPLER=tex the texture gather for every launch.
-    ctx->sampler = 2;
+    ctx->sampler = 3;  // auto: TMA tiles for the T0 launches where they pay, the texture gather otherwise
     const char* smp = std::getenv("TT_SAMPLER");
     if (smp && (std::strcmp(smp, "ldg") == 0 || std::strcmp(smp, "0") == 0)) ctx->sampler = 0;
     if (smp && (std::strcmp(smp, "tex") == 0 || std::strcmp(smp, "1") == 0)) ctx->sampler = 1;
@@ -727,8 +728,8 @@ tt_status tt_ctx_device(const tt_ctx* ctx, int* out) {
 
 tt_status tt_ctx_set_sampler(tt_ctx* ctx, int sampler) {
     TT_CHECK_CTX(ctx);
-    if (sampler < 0 || sampler > 2)
-        return fail(ctx, TT_ERR_INVALID, "sampler must be 0 (global), 1 (texture) or 2 (TMA tiles, T0)");
+    if (sampler < 0 || sampler > 3)
+        return fail(ctx, TT_ERR_INVALID, "sampler must be 0 (global), 1 (texture), 2 (TMA tiles, T0) or 3 (auto)");
     ctx->sampler = sampler;
     return TT_OK;
 }

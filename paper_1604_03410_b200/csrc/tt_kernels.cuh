@@ -52,6 +52,8 @@ struct TraceArgs {
 
 // True when launch_trace serves a Sampler::Tma launch with the TMA tile kernel itself.
 bool tma_radon_ok(const TraceArgs& a);
+// ... and worth it: enough taps (units * n^2) to amortise its per-launch cost (the context's default sampler)
+bool tma_radon_pays(const TraceArgs& a);
 // Size (ints) of the fused P stage's state for a launch: per unit a line counter and a finished-row
 // counter (zeroed once; every launch leaves them zeroed).
 std::size_t epi_state_ints(const TraceArgs& a);

@@ -95,7 +95,9 @@ class ShardedTrace:
         self.device = torch.device("cuda", device)
         if sampler is None:  # the measured-faster sampler: TMA tiles for the T0 launches they serve, else texture
             from .trace import schedule_slots
-            tma = not full and n > 704 and n % 4 == 0 and schedule_slots(n, False) == 32
+            units = min(shard.orientation_shard(angles, self.world, r)[1] for r in range(self.world))
+            tma = (not full and n > 704 and n % 4 == 0 and schedule_slots(n, False) == 32
+                   and (units // self.chunks) * n * n >= 1.5e8)  # tiles pay from ~1.5e8 taps per launch
             sampler = 2 if tma else 1
         self.sampler = sampler
         dev = self.device

@@ -67,7 +67,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--sampler", default="auto", choices=["auto", "tex", "tma"],
-                    help="auto (the product default): TMA tiles for the T0 launches they serve, texture otherwise")
+                    help="auto (the product default): TMA tiles for the T0 launches they serve of >= 1.5e8 taps, texture otherwise")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     flush = torch.empty(int(256 << 20) // 4, device="cuda")
@@ -83,7 +83,8 @@ def main():
                 if full and n > tt.max_full_n():
                     continue
                 reps = 5 if n * n * A > 4e10 else 10
-                tma_ok = not full and n > 704 and n % 4 == 0  # the product rule for these (power-of-two) n
+                # the product rule (context sampler 3) for these (power-of-two) n: tiles from 1.5e8 taps
+                tma_ok = not full and n > 704 and n % 4 == 0 and (A // 2) * n * n >= 1.5e8
                 smp = 2 if (args.sampler == "tma" or (args.sampler == "auto" and tma_ok)) else 1
                 pt = run_point(n, A, full, stream, flush, reps, peak, tpeak, smp)
                 pt["fp32_peak_tflops"] = peak

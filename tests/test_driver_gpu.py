@@ -267,22 +267,22 @@ def test_trace_launch_contract(ctx):
 
 
 def test_sampler_selection_contract(gpu):
-    """tt_ctx_set_sampler: 0 (L1 loads), 1 (texture), 2 (TMA tiles for the T0 launches they serve, the
-    default); anything else is TT_ERR_INVALID and leaves the sampler unchanged.  Every sampler gives the
-    same bits."""
+    """tt_ctx_set_sampler: 0 (L1 loads), 1 (texture), 2 (TMA tiles for the T0 launches they serve), 3
+    (the default: tiles where they pay); anything else is TT_ERR_INVALID and leaves the sampler unchanged.
+    Every sampler gives the same bits."""
     n, A = 1024, 4
     img = tt.synth_image(tt.PHANTOM, n)
     ctx = tt.create_context(gpu)
     try:
         outs = []
-        for smp in (2, 1, 0):
-            if smp != 2:
+        for smp in (3, 2, 1, 0):
+            if smp != 3:
                 ctx.set_sampler(smp)
             out, _, rep = tt.TraceTransform(ctx, n, A, full=False)(img)
             assert rep.ok()
             outs.append(out.reshape(-1).view(np.uint32))
         assert all(np.array_equal(outs[0], o) for o in outs[1:])
-        for bad in (-1, 3, 7):
+        for bad in (-1, 4, 7):
             with pytest.raises(tt.api.AbiError):
                 ctx.set_sampler(bad)
     finally:

@@ -35,7 +35,8 @@ def _worker(rank, world, port, n, A, chunks, result, full=True, assembly="p2p"):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     F = 6 if full else 1
-    st = ShardedTrace(n, A, dist, 0, chunks=chunks, full=full, assembly=assembly)  # T0 at n > 768: TMA tiles
+    # T0 at n > 704: the TMA tile kernel (explicitly: the default keeps launches this short on TLD4)
+    st = ShardedTrace(n, A, dist, 0, chunks=chunks, full=full, assembly=assembly, sampler=None if full else 2)
     ok = st.assembly == assembly
     imgs = [tt.synth_image(kind, n) for kind in (tt.PHANTOM, tt.DISK, tt.SPARSE)]
     root = rank == 0
