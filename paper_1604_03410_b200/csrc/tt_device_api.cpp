@@ -323,12 +323,18 @@ tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, std::int64_t
                 t->tex = v.second;
                 return TT_OK;
             }
-        if (!tt::pitch_texture_ok(d_imgs, t->n)) return fail(nullptr, TT_ERR_INVALID, "image not texture-aligned");
-        cudaArray_t none = nullptr;
+        cudaArray_t arr = nullptr;
         cudaTextureObject_t tex = 0;
-        e = tt::make_image_texture(d_imgs, t->n, (cudaStream_t)stream, &none, &tex);
-        if (e != cudaSuccess) return cuda_fail(nullptr, e, "image texture view");
-        t->views.emplace_back(d_imgs, tex);  // kept until destroy: earlier launches may still use the others
+        e = tt::make_image_texture(d_imgs, t->n, (cudaStream_t)stream, &arr, &tex);  // a view, or an array copy
+        if (e != cudaSuccess) {                                                     // of an unaligned image
+            if (arr) cudaFreeArray(arr);
+            return cuda_fail(nullptr, e, "image texture view");
+        }
+        if (arr) {
+            t->arr = arr;  // from now on an array-backed handle (later updates copy into it)
+        } else {
+            t->views.emplace_back(d_imgs, tex);  // kept until destroy: earlier launches may still use the others
+        }
         t->tex = tex;
         return TT_OK;
     }
@@ -342,11 +348,12 @@ tt_status tt_image_tex_update(tt_image_tex* t, const float* d_imgs, std::int64_t
 
 tt_status tt_image_tex_destroy(tt_image_tex* t) {
     if (!t) return TT_OK;
-    if (t->views.empty()) {
-        cudaDestroyTextureObject(t->tex);
-    } else {
-        for (const auto& v : t->views) cudaDestroyTextureObject(v.second);
+    bool tex_is_view = false;
+    for (const auto& v : t->views) {
+        cudaDestroyTextureObject(v.second);
+        tex_is_view |= v.second == t->tex;
     }
+    if (!tex_is_view) cudaDestroyTextureObject(t->tex);
     if (t->arr) cudaFreeArray(t->arr);
     delete t;
     return TT_OK;

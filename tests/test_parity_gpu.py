@@ -210,6 +210,18 @@ def test_texture_handle_follows_images(ctx, n):
             host = imgs[k].cpu().numpy()
             ro, rm = O.replay_launch(host, n, c, s, w, a0=0, units=8, pair_stride=0)
             assert _bitwise_equal(out.cpu().numpy(), ro) and np.array_equal(med.cpu().numpy(), rm), (step, k)
+        # an image that is not texture-aligned (4 bytes into a buffer): the handle falls back to an array copy
+        buf = torch.zeros(n * n + 1, device="cuda")
+        buf[1:].copy_(imgs[1].reshape(-1))
+        odd = buf[1:].view(n, n)
+        tt.trace.image_texture_update(tex, odd.data_ptr())
+        out = torch.empty((8, 6, n), device="cuda")
+        med = torch.empty((8, 2, n), dtype=torch.int32, device="cuda")
+        tt.trace_device(odd.data_ptr(), n, 0, 8, ct.data_ptr(), st.data_ptr(), wt.data_ptr(), out.data_ptr(),
+                        med.data_ptr(), sampler=1, tex=tex, pair_stride=-1)
+        torch.cuda.synchronize()
+        ro, rm = O.replay_launch(odd.cpu().numpy(), n, c, s, w, a0=0, units=8, pair_stride=0)
+        assert _bitwise_equal(out.cpu().numpy(), ro) and np.array_equal(med.cpu().numpy(), rm), "unaligned"
     finally:
         tt.trace.image_texture_destroy(tex)
 
